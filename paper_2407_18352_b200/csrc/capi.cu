@@ -1,0 +1,303 @@
+// extern "C" entry points of libsmlrt_b200 (declared in include/smlrt_b200.h).
+// Dispatch only: validation, device tables, and the choice of kernel.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+using namespace smlrt;
+
+namespace {
+
+int device_tables(smlrt_plan_t p, DevPlan* d, const int32_t* dtypes, int n) {
+  int rc = p->tables(d);
+  if (rc) return rc;
+  d->all_f32 = 1;
+  for (int i = 0; i < n; ++i) d->all_f32 &= dtypes[i] == SMLRT_F32;
+  return SMLRT_OK;
+}
+
+struct Scratch {  // stream-ordered temporary
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  int alloc(size_t bytes) {
+    if (bytes == 0) return SMLRT_OK;
+    SMLRT_CUDA(cudaMallocAsync(&p, bytes, s));
+    return SMLRT_OK;
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+int check_rows(smlrt_plan_t p, int64_t r0, int64_t r1) {
+  if (r0 < 0 || r1 > p->n_rows || r0 > r1)
+    return fail(SMLRT_E_INVALID, "row range [" + std::to_string(r0) + "," + std::to_string(r1) +
+                                     ") outside the plan's " + std::to_string(p->n_rows) + " rows");
+  return SMLRT_OK;
+}
+
+}  // namespace
+
+smlrt_model_s::~smlrt_model_s() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  for (auto& L : layers) {
+    cudaFree(L.w);
+    cudaFree(L.b);
+  }
+  cudaFree(tc_blob);
+  cudaSetDevice(prev);
+}
+
+extern "C" int smlrt_model_upload(const smlrt_layer_t* layers, int n_layers, int precision,
+                                  int device, smlrt_model_t* out) {
+  if (!layers || n_layers < 1 || !out) return fail(SMLRT_E_INVALID, "model_upload: no layers");
+  if (precision != SMLRT_FP32_EXACT && precision != SMLRT_BF16)
+    return fail(SMLRT_E_INVALID, "model_upload: unknown precision");
+  for (int l = 0; l < n_layers; ++l) {
+    const auto& L = layers[l];
+    if (L.in < 1 || L.out < 1 || !L.weights || !L.bias)
+      return fail(SMLRT_E_INVALID, "model_upload: empty layer " + std::to_string(l));
+    if (L.activation < SMLRT_IDENTITY || L.activation > SMLRT_TANH)
+      return fail(SMLRT_E_INVALID, "model_upload: unknown activation");
+    if (l && L.in != layers[l - 1].out)
+      return fail(SMLRT_E_MODEL_SHAPE, "model_upload: layer chain breaks at " + std::to_string(l));
+  }
+  int prev = 0;
+  SMLRT_CUDA(cudaGetDevice(&prev));
+  SMLRT_CUDA(cudaSetDevice(device));
+  auto* m = new smlrt_model_s();
+  m->precision = precision;
+  m->device = device;
+  m->n_layers = n_layers;
+  m->in_features = layers[0].in;
+  m->out_features = layers[n_layers - 1].out;
+  m->max_width = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    const auto& L = layers[l];
+    DevLayer d;
+    d.in = L.in;
+    d.out = L.out;
+    d.act = L.activation;
+    size_t nw = (size_t)L.in * L.out;
+    m->max_width = std::max(m->max_width, std::max(L.in, L.out));
+    if (cudaMalloc(&d.w, nw * 4) != cudaSuccess || cudaMalloc(&d.b, (size_t)L.out * 4) != cudaSuccess ||
+        cudaMemcpy(d.w, L.weights, nw * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d.b, L.bias, (size_t)L.out * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      m->layers.push_back(d);
+      delete m;
+      cudaSetDevice(prev);
+      return fail(SMLRT_E_CUDA, "model_upload: device allocation/copy failed");
+    }
+    m->layers.push_back(d);
+    m->host_params.insert(m->host_params.end(), L.weights, L.weights + nw);
+    m->host_params.insert(m->host_params.end(), L.bias, L.bias + L.out);
+  }
+  if (precision == SMLRT_BF16) {
+    int rc = tc_pack_model(*m);
+    if (rc) {
+      std::string msg = smlrt_last_error();
+      delete m;
+      cudaSetDevice(prev);
+      return fail(rc, msg);
+    }
+  }
+  cudaSetDevice(prev);
+  *out = m;
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_model_free(smlrt_model_t m) {
+  delete m;
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_model_path(smlrt_model_t m, int32_t n_in_cols, int32_t* path) {
+  if (!m || !path) return fail(SMLRT_E_INVALID, "model_path: null");
+  (void)n_in_cols;
+  DevPlan dummy{};
+  *path = 2;
+  if (m->precision == SMLRT_BF16) {
+    if (launch_region_tc(*m, dummy, nullptr, nullptr, 0, dummy, nullptr, nullptr, 0, 0, 0, nullptr,
+                         0, nullptr, true) == SMLRT_OK)
+      *path = 3;
+    else
+      *path = 0;
+  } else if (launch_region_exact_fused(*m, dummy, nullptr, nullptr, 0, dummy, nullptr, nullptr, 0, 0,
+                                       0, nullptr, 0, nullptr, true) == SMLRT_OK) {
+    *path = 1;
+  }
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_gather(smlrt_plan_t p, const void* const* ptrs, const int32_t* dts, void* out,
+                            int32_t out_dtype, int64_t r0, int64_t r1, void* stream) {
+  if (!p || !ptrs || !dts || !out) return fail(SMLRT_E_INVALID, "gather: null argument");
+  if (int rc = check_rows(p, r0, r1)) return rc;
+  DevPlan d;
+  if (int rc = device_tables(p, &d, dts, p->n_arrays)) return rc;
+  return launch_gather(d, ptrs, dts, p->n_arrays, out, out_dtype, r0, r1, (cudaStream_t)stream);
+}
+
+extern "C" int smlrt_scatter(smlrt_plan_t p, const void* in, int32_t in_dtype, void* const* ptrs,
+                             const int32_t* dts, int64_t r0, int64_t r1, void* stream) {
+  if (!p || !ptrs || !dts || !in) return fail(SMLRT_E_INVALID, "scatter: null argument");
+  if (p->direction != SMLRT_FROM) return fail(SMLRT_E_INVALID, "scatter needs a FROM plan");
+  if (int rc = check_rows(p, r0, r1)) return rc;
+  DevPlan d;
+  if (int rc = device_tables(p, &d, dts, p->n_arrays)) return rc;
+  return launch_scatter(d, in, in_dtype, ptrs, dts, p->n_arrays, r0, r1, (cudaStream_t)stream,
+                        nullptr);
+}
+
+namespace {
+
+// Layer-by-layer exact forward over dense f32 rows; ping-pong buffers.
+int forward_unfused(const smlrt_model_s& m, const float* x, int64_t rows, float* y, float* t0,
+                    float* t1, cudaStream_t s, uint32_t* status) {
+  const float* cur = x;
+  for (int l = 0; l < m.n_layers; ++l) {
+    bool last = l == m.n_layers - 1;
+    float* dst = last ? y : (l % 2 ? t1 : t0);
+    if (int rc = launch_dense_exact(cur, rows, m.layers[l], dst, s, last ? status : nullptr)) return rc;
+    cur = dst;
+  }
+  return SMLRT_OK;
+}
+
+constexpr int64_t kChunk = 1 << 16;  // rows per unfused chunk (bounds scratch)
+
+}  // namespace
+
+extern "C" int smlrt_infer(smlrt_model_t m, const void* x, int32_t x_dtype, int64_t rows, void* y,
+                           int32_t y_dtype, void* stream, uint32_t* status) {
+  if (!m || !x || !y || !status) return fail(SMLRT_E_INVALID, "infer: null argument");
+  if (rows <= 0) return SMLRT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t ch = std::min(rows, kChunk);
+  Scratch sc(s);
+  size_t per = (size_t)m->in_features + 2 * (size_t)m->max_width + m->out_features;
+  if (int rc = sc.alloc(per * ch * 4)) return rc;
+  float* xin = (float*)sc.p;
+  float* t0 = xin + ch * m->in_features;
+  float* t1 = t0 + ch * m->max_width;
+  float* yo = t1 + ch * m->max_width;
+  size_t xs = x_dtype == SMLRT_F32 ? 4 : 8, ys = y_dtype == SMLRT_F32 ? 4 : 8;
+  for (int64_t r = 0; r < rows; r += ch) {
+    int64_t n = std::min(ch, rows - r);
+    const char* xp = (const char*)x + r * m->in_features * xs;
+    if (int rc = launch_convert(xp, x_dtype, xin, SMLRT_F32, n * m->in_features, s)) return rc;
+    if (int rc = forward_unfused(*m, xin, n, yo, t0, t1, s, status)) return rc;
+    char* yp = (char*)y + r * m->out_features * ys;
+    if (int rc = launch_convert(yo, SMLRT_F32, yp, y_dtype, n * m->out_features, s)) return rc;
+  }
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_region_workspace(smlrt_plan_t in, smlrt_plan_t out, smlrt_model_t m, int64_t rows,
+                                      int32_t flags, size_t* bytes) {
+  if (!in || !out || !m || !bytes) return fail(SMLRT_E_INVALID, "region_workspace: null");
+  size_t b = 0;
+  if (flags & SMLRT_COMMIT_CHECKED) b += (size_t)rows * m->out_features * 4;
+  *bytes = b;
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_region_infer(smlrt_plan_t pin, const void* const* in_ptrs, const int32_t* in_dt,
+                                  smlrt_plan_t pout, void* const* out_ptrs, const int32_t* out_dt,
+                                  smlrt_model_t m, int64_t r0, int64_t r1, int32_t flags,
+                                  void* workspace, void* stream, uint32_t* status) {
+  if (!pin || !pout || !m || !in_ptrs || !out_ptrs || !in_dt || !out_dt || !status)
+    return fail(SMLRT_E_INVALID, "region_infer: null argument");
+  if (pin->direction != SMLRT_TO || pout->direction != SMLRT_FROM)
+    return fail(SMLRT_E_INVALID, "region_infer: plans have the wrong directions");
+  // runtime.py:327-338
+  if (pin->n_cols != m->in_features)
+    return fail(SMLRT_E_MODEL_SHAPE, "region gathers " + std::to_string(pin->n_cols) +
+                                         " features, model expects " + std::to_string(m->in_features));
+  if (pout->n_cols != m->out_features)
+    return fail(SMLRT_E_MODEL_SHAPE, "region scatters " + std::to_string(pout->n_cols) +
+                                         " features, model emits " + std::to_string(m->out_features));
+  if (pout->n_rows != pin->n_rows)
+    return fail(SMLRT_E_MODEL_SHAPE, "output map sweeps " + std::to_string(pout->n_rows) +
+                                         " entries, batch holds " + std::to_string(pin->n_rows));
+  if (int rc = check_rows(pin, r0, r1)) return rc;
+  if (r1 == r0) return SMLRT_OK;
+  int dev = 0;
+  SMLRT_CUDA(cudaGetDevice(&dev));
+  if (dev != m->device) return fail(SMLRT_E_INVALID, "region_infer: model lives on another device");
+  cudaStream_t s = (cudaStream_t)stream;
+  DevPlan din, dout;
+  if (int rc = device_tables(pin, &din, in_dt, pin->n_arrays)) return rc;
+  if (int rc = device_tables(pout, &dout, out_dt, pout->n_arrays)) return rc;
+  int64_t rows = r1 - r0;
+  bool checked = flags & SMLRT_COMMIT_CHECKED;
+  Scratch stage_sc(s);
+  float* staged = nullptr;
+  if (checked) {
+    if (workspace) {
+      staged = (float*)workspace;
+    } else {
+      if (int rc = stage_sc.alloc((size_t)rows * m->out_features * 4)) return rc;
+      staged = (float*)stage_sc.p;
+    }
+  }
+  int rc = SMLRT_E_UNSUPPORTED;
+  if (!(flags & SMLRT_FORCE_UNFUSED)) {
+    if (m->precision == SMLRT_BF16)
+      rc = launch_region_tc(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt,
+                            pout->n_arrays, r0, r1, staged, s, status, false);
+    else
+      rc = launch_region_exact_fused(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt,
+                                     pout->n_arrays, r0, r1, staged, s, status, false);
+    if (rc != SMLRT_OK && rc != SMLRT_E_UNSUPPORTED) return rc;
+    if (rc == SMLRT_E_UNSUPPORTED && m->precision == SMLRT_BF16)
+      return fail(SMLRT_E_UNSUPPORTED, "no tcgen05 kernel for this model shape");
+  }
+  if (rc == SMLRT_E_UNSUPPORTED) {
+    // unfused exact path: gather -> per-layer kernels -> scatter, chunked
+    int64_t ch = std::min(rows, kChunk);
+    Scratch sc(s);
+    size_t per = (size_t)m->in_features + 2 * (size_t)m->max_width + m->out_features;
+    if (int e = sc.alloc(per * ch * 4)) return e;
+    float* xin = (float*)sc.p;
+    float* t0 = xin + ch * m->in_features;
+    float* t1 = t0 + ch * m->max_width;
+    float* yo = t1 + ch * m->max_width;
+    for (int64_t r = r0; r < r1; r += ch) {
+      int64_t n = std::min(ch, r1 - r);
+      if (int e = launch_gather(din, in_ptrs, in_dt, pin->n_arrays, xin, SMLRT_F32, r, r + n, s)) return e;
+      float* ydst = checked ? staged + (r - r0) * m->out_features : yo;
+      if (int e = forward_unfused(*m, xin, n, ydst, t0, t1, s, status)) return e;
+      if (!checked)
+        if (int e = launch_scatter(dout, ydst, SMLRT_F32, out_ptrs, out_dt, pout->n_arrays, r, r + n, s,
+                                   nullptr))
+          return e;
+    }
+  }
+  if (checked) {
+    // commit: a no-op on device when the status word is non-zero
+    if (int e = launch_scatter(dout, staged, SMLRT_F32, out_ptrs, out_dt, pout->n_arrays, r0, r1, s,
+                               status))
+      return e;
+  }
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_collect_async(const void* dense_dev, size_t bytes, void* pinned_host,
+                                   void* side_stream, void* after_event) {
+  if (!dense_dev || !pinned_host) return fail(SMLRT_E_INVALID, "collect_async: null argument");
+  cudaStream_t s = (cudaStream_t)side_stream;
+  if (after_event) SMLRT_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)after_event, 0));
+  SMLRT_CUDA(cudaMemcpyAsync(pinned_host, dense_dev, bytes, cudaMemcpyDeviceToHost, s));
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_collect_wait(void* side_stream) {
+  SMLRT_CUDA(cudaStreamSynchronize((cudaStream_t)side_stream));
+  return SMLRT_OK;
+}

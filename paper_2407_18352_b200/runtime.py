@@ -1,0 +1,529 @@
+"""Execution control: the reference's Runtime API over the B200 data path.
+
+Same registry, dispatch, caches, outcome/stats records and error classes as
+`/root/reference/pkg/src/smlrt/runtime.py:129-398`.  What changes is the body
+of the two data paths:
+
+* `_run_surrogate` (runtime.py:308-370) validates the maps on the host, looks
+  up (or compiles once) the gather and scatter plans, and issues ONE native
+  call, `smlrt_region_infer`: gather -> forward pass -> scatter fused in a
+  single sm_100a kernel (fp32-exact CUDA-core or bf16 tcgen05 by model
+  precision).  The only device->host traffic is the 4-byte status word.
+* `_run_collect` (runtime.py:279-306) gathers the inputs with the native
+  gather kernel into HBM, copies the dense tile to pinned host memory on a
+  side stream (`smlrt_collect_async`), runs the accurate callback, gathers the
+  outputs the same way and appends the record to the SRDB store.
+
+Application arrays normally live in HBM.  A host-resident ArrayBuffer is
+staged through a cached device mirror (H2D before, D2H of written outputs
+after): that is the end-to-end path the bench times with host buffers.
+
+Sharding: `Runtime(shard=(rank, world))` restricts every invocation to the
+rank's contiguous block of flattened sweep rows (axis 0 blocks for row-major
+sweeps); there is no collective on the inference path.
+
+A Runtime instance belongs to one thread of control (runtime.py:22).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field, replace
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native, srdb
+from .bridge import (
+    ArrayBuffer,
+    DTYPE_CODE,
+    Plan,
+    Tensor,
+    _check_features,
+    _views_for,
+    build_plan,
+    check_scatter_functor,
+    expected_tensor_shape,
+)
+from .directives import FunctorDecl, MapTarget, MlDirective
+from .errors import (
+    DuplicateRegionError,
+    InvalidScheduleError,
+    MissingClauseError,
+    MissingPredicateError,
+    ModelLoadError,
+    ModelShapeMismatchError,
+    NonFiniteOutputError,
+    ShapeMismatchError,
+    UnknownRegionError,
+)
+from .models import Model, device_model, load_model
+
+__all__ = ["BoundMap", "RegionDescriptor", "RegionOutcome", "RegionStats", "Runtime",
+           "interleave_predicate"]
+
+ACCURATE = "accurate"
+SURROGATE = "surrogate"
+
+
+@dataclass
+class BoundMap:
+    functor: FunctorDecl
+    target: MapTarget
+    array: ArrayBuffer
+
+
+@dataclass
+class RegionDescriptor:
+    name: str
+    accurate_fn: Callable[[], None]
+    ml: MlDirective
+    in_maps: list = field(default_factory=list)
+    out_maps: list = field(default_factory=list)
+    inout_maps: list = field(default_factory=list)
+    env: dict = field(default_factory=dict)
+
+
+@dataclass
+class RegionOutcome:
+    """elapsed_region_ns: the executed body (accurate callback, or the fused
+    surrogate launch through its completion).  On the fused path map_to covers
+    host validation + plan lookup and map_from the status check; the device
+    work of gather and scatter is inside the infer interval."""
+
+    path_taken: str
+    elapsed_region_ns: int
+    elapsed_map_to_ns: int = 0
+    elapsed_map_from_ns: int = 0
+    elapsed_infer_ns: int = 0
+    record_index: Optional[int] = None
+
+
+@dataclass
+class RegionStats:
+    invocations: int = 0
+    accurate_calls: int = 0
+    surrogate_calls: int = 0
+    records: int = 0
+    model_loads: int = 0
+    map_to_ns: int = 0
+    map_from_ns: int = 0
+    infer_ns: int = 0
+    accurate_ns: int = 0
+
+
+def interleave_predicate(step: int, n_accurate: int, n_surrogate: int) -> bool:
+    """True on the surrogate part of a repeating n_accurate:n_surrogate schedule."""
+    if n_accurate < 0 or n_surrogate < 0:
+        raise InvalidScheduleError("interleave counts must be non-negative")
+    period = n_accurate + n_surrogate
+    if period == 0:
+        raise InvalidScheduleError("interleave schedule needs a non-zero period")
+    return (step % period) >= n_accurate
+
+
+def _resolve_refs(refs: Sequence[str], maps: Sequence[BoundMap], clause: str):
+    names = {}
+    for m in maps:
+        if m.target.array in names:
+            raise MissingClauseError(f"array {m.target.array!r} bound twice in {clause} maps")
+        names[m.target.array] = m
+    for r in refs:
+        if r not in names:
+            raise MissingClauseError(f"ml {clause}({r}) has no matching bound map")
+
+
+def _ns_since(t0: int) -> int:
+    return max(time.perf_counter_ns() - t0, 1)
+
+
+def _shard_rows(n_rows: int, shard) -> tuple[int, int]:
+    if shard is None:
+        return 0, n_rows
+    rank, world = shard
+    per = -(-n_rows // world)
+    return min(rank * per, n_rows), min((rank + 1) * per, n_rows)
+
+
+class _Staging:
+    """Device mirrors of host-resident ArrayBuffers (the e2e path)."""
+
+    def __init__(self):
+        self._mirror: dict[int, tuple[torch.Tensor, ArrayBuffer]] = {}
+
+    def device_view(self, a: ArrayBuffer, device: torch.device) -> ArrayBuffer:
+        if a.is_device:
+            return a
+        key = id(a.data)
+        hit = self._mirror.get(key)
+        if hit is None or hit[0].numel() != a.data.numel() or hit[0].dtype != a.data.dtype:
+            t = torch.empty(a.data.numel(), dtype=a.data.dtype, device=device)
+            hit = (t, ArrayBuffer(t, a.shape, a.strides))
+            self._mirror[key] = hit
+        return hit[1]
+
+    def upload(self, a: ArrayBuffer, dev_a: ArrayBuffer):
+        if dev_a is not a:
+            dev_a.data.copy_(a.data, non_blocking=a.data.is_pinned())
+
+    def download(self, a: ArrayBuffer, dev_a: ArrayBuffer):
+        if dev_a is not a:
+            a.data.copy_(dev_a.data, non_blocking=a.data.is_pinned())
+
+
+class Runtime:
+    """Registry of annotated regions plus model, plan and database caches.
+
+    precision: override every model's precision ("fp32" exact | "bf16").
+    commit:    "fused" (outputs written from the kernel epilogue) or "checked"
+               (staged; nothing written if the output is non-finite, the
+               reference's error-before-write order, runtime.py:341-344).
+    shard:     (rank, world) row block processed by this instance.
+    """
+
+    def __init__(self, precision: Optional[str] = None, commit: str = "fused",
+                 shard: Optional[tuple[int, int]] = None, device=None):
+        if commit not in ("fused", "checked"):
+            raise ValueError("commit must be 'fused' or 'checked'")
+        self._regions: dict[str, RegionDescriptor] = {}
+        self._stats: dict[str, RegionStats] = {}
+        self._models: dict[str, Model] = {}
+        self._dbs: dict[str, srdb.SrdbDatabase] = {}
+        self._plans: dict[str, tuple] = {}
+        self._staging = _Staging()
+        self.precision = precision
+        self.commit = commit
+        self.shard = shard
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else None)
+        self._status = None
+        # bench/profiling hook: CUDA events around each fused launch, on its stream
+        self.time_kernels = False
+        self.kernel_events: list = []
+
+    # -- registration ---------------------------------------------------------
+
+    def register_region(self, desc: RegionDescriptor) -> str:
+        ml = desc.ml
+        if ml.mode in ("infer", "predicated") and not ml.model_path:
+            raise MissingClauseError(f"ml({ml.mode}) region without a model path")
+        if ml.mode in ("collect", "predicated") and not ml.db_path:
+            raise MissingClauseError(f"ml({ml.mode}) region without a db path")
+        _resolve_refs(ml.in_refs, desc.in_maps, "in")
+        _resolve_refs(ml.out_refs, desc.out_maps, "out")
+        _resolve_refs(ml.inout_refs, desc.inout_maps, "inout")
+        prev = self._regions.get(desc.name)
+        if prev is not None:
+            if prev != desc:
+                raise DuplicateRegionError(
+                    f"region {desc.name!r} already registered with a different descriptor")
+            return desc.name
+        self._regions[desc.name] = desc
+        self._stats[desc.name] = RegionStats()
+        return desc.name
+
+    def _region(self, handle: str) -> RegionDescriptor:
+        try:
+            return self._regions[handle]
+        except KeyError:
+            raise UnknownRegionError(f"no region registered as {handle!r}") from None
+
+    # -- caches ---------------------------------------------------------------
+
+    def _model_for(self, desc: RegionDescriptor) -> Model:
+        key = os.path.realpath(desc.ml.model_path)
+        m = self._models.get(key)
+        if m is None:
+            try:
+                m = load_model(desc.ml.model_path)
+            except Exception as e:
+                raise ModelLoadError(f"cannot load model {desc.ml.model_path!r}: {e}") from e
+            self._models[key] = m
+            self._stats[desc.name].model_loads += 1
+        return m
+
+    def _db_for(self, desc: RegionDescriptor) -> srdb.SrdbDatabase:
+        path = desc.ml.db_path
+        db = self._dbs.get(path)
+        if db is None:
+            exists = os.path.exists(os.path.join(path, srdb.MANIFEST_NAME))
+            db = srdb.open_db(path, "append" if exists else "create")
+            self._dbs[path] = db
+        return db
+
+    def unload_models(self):
+        """Drop cached models; the next inference reloads from disk."""
+        self._models.clear()
+
+    def close(self):
+        for db in self._dbs.values():
+            db.close()
+        self._dbs.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _status_word(self) -> torch.Tensor:
+        if self._status is None:
+            self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        return self._status
+
+    # -- invocation -----------------------------------------------------------
+
+    def invoke_region(self, handle: str, predicate_value: Optional[bool] = None,
+                      if_value: Optional[bool] = None) -> RegionOutcome:
+        desc = self._region(handle)
+        st = self._stats[handle]
+        st.invocations += 1
+        ml = desc.ml
+        if ml.if_cond is not None:
+            if if_value is None:
+                raise MissingPredicateError(
+                    f"region {handle!r} has an if({ml.if_cond}) clause; pass if_value on every invocation")
+            if not if_value:
+                return self._run_plain_accurate(desc, st)
+        if ml.mode == "collect":
+            surrogate = False
+        elif ml.mode == "infer":
+            surrogate = True
+        else:
+            if predicate_value is None:
+                raise MissingPredicateError(
+                    f"region {handle!r} is predicated ({ml.predicate}); pass predicate_value on every invocation")
+            surrogate = bool(predicate_value)
+        return self._run_surrogate(desc, st) if surrogate else self._run_collect(desc, st)
+
+    # -- paths ----------------------------------------------------------------
+
+    def _sync(self):
+        if self.device is not None:
+            torch.cuda.current_stream(self.device).synchronize()
+
+    def _run_plain_accurate(self, desc, st) -> RegionOutcome:
+        self._sync()
+        t0 = time.perf_counter_ns()
+        desc.accurate_fn()
+        self._sync()
+        dt = _ns_since(t0)
+        st.accurate_calls += 1
+        st.accurate_ns += dt
+        return RegionOutcome(path_taken=ACCURATE, elapsed_region_ns=dt)
+
+    def _device_maps(self, maps):
+        out = []
+        for m in maps:
+            if m.array.is_device:
+                out.append(m)
+            else:
+                if self.device is None:
+                    raise RuntimeError("no CUDA device: the B200 runtime has no CPU data path")
+                out.append(BoundMap(m.functor, m.target,
+                                    self._staging.device_view(m.array, self.device)))
+        return out
+
+    def _gather_dense(self, maps) -> Tensor:
+        """_combined_tensor (runtime.py:379-398) on the device."""
+        if not maps:
+            raise MissingClauseError("region has no maps for this direction")
+        groups, sweep = [], None
+        for m in maps:
+            views = _views_for(m.functor, m.target, m.array)
+            s = _check_features(views, m.functor)
+            if sweep is None:
+                sweep = s
+            elif s != sweep:
+                raise ShapeMismatchError(f"map over {m.target.array!r} sweeps {s}, expected {sweep}")
+            groups.append(views)
+        dt = "f64" if any(m.array.dtype == "f64" for m in maps) else "f32"
+        plan = build_plan(groups, "to")
+        out = torch.empty((plan.n_rows, plan.n_cols), device=self.device,
+                          dtype=torch.float32 if dt == "f32" else torch.float64)
+        ptrs, dts = plan.ptrs_and_dtypes()
+        _native.gather(plan.handle, ptrs, dts, out.data_ptr(), DTYPE_CODE[dt], 0, plan.n_rows,
+                       torch.cuda.current_stream(self.device).cuda_stream)
+        return Tensor(out.reshape(tuple(sweep) + (plan.n_cols,)))
+
+    def _snapshot(self, maps):
+        """Gather on the compute stream, copy to pinned host memory on a side stream."""
+        t = self._gather_dense(maps)
+        host = torch.empty(t.data.shape, dtype=t.data.dtype, pin_memory=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        side = self._side_stream()
+        _native.collect_async(t.data.data_ptr(), t.data.numel() * t.data.element_size(),
+                              host.data_ptr(), side.cuda_stream, ev.cuda_event)
+        return host, t
+
+    def _side_stream(self):
+        s = getattr(self, "_side", None)
+        if s is None:
+            s = self._side = torch.cuda.Stream(self.device)
+        return s
+
+    def _run_collect(self, desc, st) -> RegionOutcome:
+        in_maps = self._device_maps(desc.in_maps + desc.inout_maps)
+        out_maps = self._device_maps(desc.out_maps + desc.inout_maps)
+        t0 = time.perf_counter_ns()
+        for m, d in zip(desc.in_maps + desc.inout_maps, in_maps):
+            self._staging.upload(m.array, d.array)
+        x_host, x_dev = self._snapshot(in_maps)
+        self._sync()
+        map_to = _ns_since(t0)
+
+        t0 = time.perf_counter_ns()
+        desc.accurate_fn()
+        self._sync()
+        region_ns = _ns_since(t0)
+
+        t0 = time.perf_counter_ns()
+        for m, d in zip(desc.out_maps + desc.inout_maps, out_maps):
+            self._staging.upload(m.array, d.array)
+        y_host, y_dev = self._snapshot(out_maps)
+        _native.collect_wait(self._side_stream().cuda_stream)
+        map_from = _ns_since(t0)
+
+        index = self._db_for(desc).append_record(desc.name, x_host.numpy(), y_host.numpy(),
+                                                 region_ns)
+        st.accurate_calls += 1
+        st.accurate_ns += region_ns
+        st.map_to_ns += map_to
+        st.map_from_ns += map_from
+        st.records += 1
+        return RegionOutcome(path_taken=ACCURATE, elapsed_region_ns=region_ns,
+                             elapsed_map_to_ns=map_to, elapsed_map_from_ns=map_from,
+                             record_index=index)
+
+    def _plans_for(self, desc, in_maps, out_maps):
+        key = tuple((id(m.array.data), m.array.shape, m.array.strides, m.array.dtype,
+                     id(m.functor), m.target) for m in in_maps + out_maps)
+        hit = self._plans.get(desc.name)
+        if hit is not None and hit[0] == key:
+            return hit[1], hit[2], hit[3]
+        # in-maps: gather_batch per map in order (runtime.py:312-324)
+        groups, batch_rows = [], None
+        for m in in_maps:
+            views = _views_for(m.functor, m.target, m.array)
+            sweep = _check_features(views, m.functor)
+            rows = int(np.prod(sweep, dtype=np.int64))
+            if batch_rows is None:
+                batch_rows = rows
+            elif rows != batch_rows:
+                raise ShapeMismatchError("input maps disagree on the sweep/batch size")
+            groups.append(views)
+        pin = build_plan(groups, "to") if _same_sweeps(groups) else _flat_plan(groups, "to")
+        # out-maps: shape checks (runtime.py:344-352) then scatter_from's checks
+        ogroups = []
+        for m in out_maps:
+            shape = expected_tensor_shape(m.functor, m.target)
+            rows = int(np.prod(shape[: len(m.target.slices)], dtype=np.int64))
+            if rows != batch_rows:
+                raise ModelShapeMismatchError(
+                    f"output map over {m.target.array!r} sweeps {rows} entries, batch holds {batch_rows}")
+            check_scatter_functor(m.functor)
+            ogroups.append(_views_for(m.functor, m.target, m.array))
+        pout = build_plan(ogroups, "from") if _same_sweeps(ogroups) else _flat_plan(ogroups, "from")
+        self._plans[desc.name] = (key, pin, pout, batch_rows)
+        return pin, pout, batch_rows
+
+    def _run_surrogate(self, desc, st) -> RegionOutcome:
+        model = self._model_for(desc)
+        if self.device is None:
+            raise RuntimeError("no CUDA device: the B200 runtime has no CPU data path")
+        host_in = desc.in_maps + desc.inout_maps
+        host_out = desc.out_maps + desc.inout_maps
+        t0 = time.perf_counter_ns()
+        in_maps = self._device_maps(host_in)
+        out_maps = self._device_maps(host_out)
+        pin, pout, rows = self._plans_for(desc, in_maps, out_maps)
+        if pin.n_cols != model.input_features:
+            raise ModelShapeMismatchError(
+                f"region {desc.name!r} gathers {pin.n_cols} features, model expects {model.input_features}")
+        out_counts = sum(m.functor.feature_count for m in out_maps)
+        if out_counts != model.output_features:
+            raise ModelShapeMismatchError(
+                f"region {desc.name!r} scatters {out_counts} features, model emits {model.output_features}")
+        handle = device_model(model, self.device, self.precision)
+        for m, d in zip(host_in, in_maps):
+            self._staging.upload(m.array, d.array)
+        for m, d in zip(host_out, out_maps):
+            if not _covers(pout, d.array):
+                self._staging.upload(m.array, d.array)
+        r0, r1 = _shard_rows(rows, self.shard)
+        status = self._status_word()
+        stream = torch.cuda.current_stream(self.device)
+        map_to = _ns_since(t0)
+
+        t0 = time.perf_counter_ns()
+        status.zero_()
+        iptr, idt = pin.ptrs_and_dtypes()
+        optr, odt = pout.ptrs_and_dtypes()
+        flags = _native.COMMIT_CHECKED if self.commit == "checked" else _native.COMMIT_FUSED
+        if self.time_kernels:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(stream)
+        _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1,
+                             flags, None, stream.cuda_stream, status.data_ptr())
+        if self.time_kernels:
+            ev[1].record(stream)
+            self.kernel_events.append(ev)
+        for m, d in zip(host_out, out_maps):
+            self._staging.download(m.array, d.array)
+        bad = int(status.item())  # synchronises the stream
+        infer_ns = _ns_since(t0)
+
+        t0 = time.perf_counter_ns()
+        if bad:
+            raise NonFiniteOutputError("forward pass produced NaN/inf")
+        map_from = _ns_since(t0)
+        st.surrogate_calls += 1
+        st.map_to_ns += map_to
+        st.map_from_ns += map_from
+        st.infer_ns += infer_ns
+        return RegionOutcome(path_taken=SURROGATE, elapsed_region_ns=infer_ns,
+                             elapsed_map_to_ns=map_to, elapsed_map_from_ns=map_from,
+                             elapsed_infer_ns=infer_ns)
+
+    def stats(self, handle: str) -> RegionStats:
+        self._region(handle)
+        return replace(self._stats[handle])
+
+
+def _same_sweeps(groups) -> bool:
+    sweeps = {g[0].shape[: g[0].n_sweep] for g in groups}
+    return len(sweeps) == 1
+
+
+def _flat_plan(groups, direction):
+    """Maps with equal row counts but different sweep shapes: re-express each
+    view over a 1-D sweep when its sweep strides allow it (row-major
+    collapsible), else refuse."""
+    from .bridge import MemoryView
+    flat = []
+    for views in groups:
+        fv = []
+        for v in views:
+            sweep, strides = v.shape[: v.n_sweep], v.strides[: v.n_sweep]
+            for k in range(len(sweep) - 1):
+                if strides[k] != strides[k + 1] * sweep[k + 1]:
+                    raise ShapeMismatchError(
+                        "maps with different sweep shapes need row-major collapsible strides")
+            n = int(np.prod(sweep))
+            fv.append(MemoryView(v.source, v.base_offset, (n,) + v.shape[v.n_sweep:],
+                                 (strides[-1],) + v.strides[v.n_sweep:], 1))
+        flat.append(fv)
+    return build_plan(flat, direction)
+
+
+def _covers(plan: Plan, array: ArrayBuffer) -> bool:
+    """True when the scatter writes every element of `array` (no upload needed)."""
+    if plan.direction != "from" or len(plan.arrays) != 1:
+        return False
+    info = _native.plan_info(plan.handle)
+    return bool(info["dense_rows"]) and info["row_pitch"] == plan.n_cols and \
+        plan.n_rows * plan.n_cols == array.data.numel()

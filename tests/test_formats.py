@@ -1,0 +1,48 @@
+"""On-disk formats are byte-compatible with the reference writers (golden)."""
+
+import json
+
+import numpy as np
+
+from goldens import arrays, infer_layers, meta
+from paper_2407_18352_b200 import srdb
+from paper_2407_18352_b200.models import DenseLayer, Model, load_model, save_model
+
+
+def c1_model():
+    layers, _, _ = infer_layers("c1_options")
+    return Model(5, 1, [DenseLayer(w, b, a) for w, b, a in layers])
+
+
+def test_model_files_byte_identical(tmp_path):
+    save_model(c1_model(), tmp_path / "m")
+    assert (tmp_path / "m" / "model.json").read_text() == meta()["model_json"]
+    assert (tmp_path / "m" / "weights.bin").read_bytes() == arrays()["model_weights_bin"].tobytes()
+    m = load_model(tmp_path / "m")
+    for a, b in zip(m.layers, c1_model().layers):
+        assert a.weights.tobytes() == b.weights.tobytes() and a.activation == b.activation
+
+
+def test_bf16_hint_round_trip(tmp_path):
+    m = c1_model()
+    m.precision = "bf16"
+    save_model(m, tmp_path / "m")
+    assert json.loads((tmp_path / "m" / "model.json").read_text())["precision"] == "bf16"
+    assert load_model(tmp_path / "m").precision == "bf16"
+
+
+def test_srdb_bytes_identical(tmp_path):
+    a = arrays()
+    with srdb.open_db(tmp_path / "db", "create") as db:
+        for k in range(3):
+            assert db.append_record("stencil", a[f"srdb_x{k}"], a[f"srdb_y{k}"], 1000 + k) == k
+    for which in ("inputs.bin", "outputs.bin", "times.bin"):
+        got = (tmp_path / "db" / "regions" / "stencil" / which).read_bytes()
+        assert got == a["srdb_" + which.replace(".", "_")].tobytes(), which
+    man = json.loads((tmp_path / "db" / "manifest.json").read_text())
+    man["regions"][0]["created_utc"] = "<nondeterministic>"
+    assert man == meta()["srdb_manifest"]
+    with srdb.open_db(tmp_path / "db", "read") as db:
+        recs = db.read_records("stencil")
+        assert [r.elapsed_ns for r in recs] == [1000, 1001, 1002]
+        assert np.array_equal(recs[1].inputs.to_numpy(), a["srdb_x1"])

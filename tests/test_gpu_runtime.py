@@ -1,0 +1,225 @@
+"""Runtime semantics (the reference's tests/test_runtime.py behaviours) on
+device-resident arrays."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2407_18352_b200 as sm
+from paper_2407_18352_b200.errors import (DuplicateRegionError, MissingClauseError,
+                                          MissingPredicateError, ModelLoadError,
+                                          ModelShapeMismatchError, NonFiniteOutputError,
+                                          UnknownRegionError)
+
+pytestmark = pytest.mark.gpu
+
+IF = sm.parse_directive("functor(ifnctr: [i, j, 0:5] = ([i-1, j], [i+1, j], [i, j-1:j+2]))")
+OF = sm.parse_directive("functor(ofnctr: [i, j, 0:1] = ([i, j]))")
+ENV = {"N": 6, "M": 6}
+TO = sm.parse_directive("map(to: ifnctr(t[1:N-1, 1:M-1]))", ENV).targets[0]
+FROM = sm.parse_directive("map(from: ofnctr(tnew[1:N-1, 1:M-1]))", ENV).targets[0]
+
+
+def field(seed=0, n=6):
+    return np.random.default_rng(seed).uniform(0, 1, size=(n, n)).astype(np.float32)
+
+
+def jacobi_ref(f):
+    c = np.float32(0.25)
+    return f[:-2, 1:-1] * c + f[2:, 1:-1] * c + f[1:-1, :-2] * c + f[1:-1, 2:] * c
+
+
+def make_region(mode, db=None, model=None, if_cond=None, name="stencil"):
+    t = sm.ArrayBuffer.from_numpy(field())
+    tnew = sm.ArrayBuffer.from_numpy(field())
+    calls = []
+
+    def accurate():
+        calls.append(1)
+        f, g = t.view(), tnew.view()
+        c = 0.25
+        g[1:-1, 1:-1] = f[:-2, 1:-1] * c + f[2:, 1:-1] * c + f[1:-1, :-2] * c + f[1:-1, 2:] * c
+
+    clauses = [f"ml({mode})", "in(t)", "out(tnew)"]
+    if db:
+        clauses.append(f'db("{db}")')
+    if model:
+        clauses.append(f'model("{model}")')
+    if if_cond:
+        clauses.append(f"if({if_cond})")
+    desc = sm.RegionDescriptor(name=name, accurate_fn=accurate, ml=sm.parse_ml_clause(" ".join(clauses)),
+                               in_maps=[sm.BoundMap(IF, TO, t)], out_maps=[sm.BoundMap(OF, FROM, tnew)],
+                               env=dict(ENV))
+    return desc, t, tnew, calls
+
+
+@pytest.fixture
+def jdir(tmp_path):
+    sm.save_model(sm.jacobi_model(0.25), tmp_path / "jm")
+    return str(tmp_path / "jm")
+
+
+def test_registration(cuda, tmp_path, jdir):
+    desc, *_ = make_region("infer", model=jdir)
+    rt = sm.Runtime()
+    h = rt.register_region(desc)
+    assert rt.register_region(desc) == h
+    other, *_ = make_region("infer", model=jdir)
+    with pytest.raises(DuplicateRegionError):
+        rt.register_region(other)
+    with pytest.raises(UnknownRegionError):
+        rt.invoke_region("ghost")
+    bad, *_ = make_region("infer", model=jdir, name="x")
+    bad.in_maps = []
+    with pytest.raises(MissingClauseError):
+        rt.register_region(bad)
+
+
+def test_lazy_model_load(cuda, tmp_path):
+    desc, *_ = make_region("infer", model=str(tmp_path / "missing"))
+    rt = sm.Runtime()
+    h = rt.register_region(desc)
+    with pytest.raises(ModelLoadError):
+        rt.invoke_region(h)
+
+
+def test_surrogate_replaces_accurate_and_border_untouched(cuda, jdir):
+    desc, t, tnew, calls = make_region("infer", model=jdir)
+    before, sentinel = t.to_numpy(), tnew.to_numpy()
+    with sm.Runtime() as rt:
+        out = rt.invoke_region(rt.register_region(desc))
+    assert out.path_taken == "surrogate" and calls == [] and out.elapsed_infer_ns > 0
+    after = tnew.to_numpy()
+    assert np.array_equal(after[1:-1, 1:-1], jacobi_ref(before))  # bitwise: same op order
+    for sl in (np.s_[0, :], np.s_[-1, :], np.s_[:, 0], np.s_[:, -1]):
+        assert np.array_equal(after[sl], sentinel[sl])
+
+
+def test_model_shape_mismatch_and_cache(cuda, tmp_path, jdir):
+    bad = sm.Model(4, 1, [sm.DenseLayer(np.zeros((1, 4), np.float32), np.zeros(1, np.float32), "identity")])
+    sm.save_model(bad, tmp_path / "bad")
+    desc, *_ = make_region("infer", model=str(tmp_path / "bad"))
+    with sm.Runtime() as rt:
+        with pytest.raises(ModelShapeMismatchError):
+            rt.invoke_region(rt.register_region(desc))
+    desc, *_ = make_region("infer", model=jdir)
+    with sm.Runtime() as rt:
+        h = rt.register_region(desc)
+        rt.invoke_region(h)
+        rt.invoke_region(h)
+        assert rt.stats(h).model_loads == 1
+        rt.unload_models()
+        rt.invoke_region(h)
+        assert rt.stats(h).model_loads == 2
+
+
+def test_collect_records_bitwise(cuda, tmp_path):
+    desc, t, tnew, calls = make_region("collect", db=tmp_path / "db")
+    snaps = []
+    with sm.Runtime() as rt:
+        h = rt.register_region(desc)
+        for _ in range(5):
+            snaps.append(sm.concretize_to(IF, TO, t).to_numpy())
+            out = rt.invoke_region(h)
+            t.view().copy_(tnew.view())
+        assert rt.stats(h).records == 5 and out.record_index == 4
+    with sm.open_db(tmp_path / "db", "read") as db:
+        recs = db.read_records("stencil")
+    for r, s in zip(recs, snaps):
+        assert np.array_equal(r.inputs.to_numpy(), s) and r.elapsed_ns > 0
+    assert recs[0].outputs.shape == (4, 4, 1)
+
+
+def test_predicated_and_if_gate(cuda, tmp_path, jdir):
+    desc, _, _, calls = make_region("predicated:host", db=tmp_path / "db", model=jdir)
+    with sm.Runtime() as rt:
+        h = rt.register_region(desc)
+        paths = [rt.invoke_region(h, predicate_value=v).path_taken for v in [False, False, True, False, True]]
+        st = rt.stats(h)
+        with pytest.raises(MissingPredicateError):
+            rt.invoke_region(h)
+    assert paths == ["accurate", "accurate", "surrogate", "accurate", "surrogate"]
+    assert st.records == 3 and st.surrogate_calls == 2 and len(calls) == 3
+    desc, _, _, calls = make_region("infer", model=jdir, if_cond="enabled", name="gated")
+    with sm.Runtime() as rt:
+        h = rt.register_region(desc)
+        assert rt.invoke_region(h, if_value=False).path_taken == "accurate"
+        assert rt.invoke_region(h, if_value=True).path_taken == "surrogate"
+        assert calls == [1]
+
+
+def test_inout_snapshot_collect(cuda, tmp_path):
+    state = sm.ArrayBuffer.from_numpy(np.arange(8, dtype=np.float64))
+    f = sm.parse_directive("functor(f: [k, 0:1] = ([k]))")
+    t = sm.parse_directive("map(to: f(state[0:8]))").targets[0]
+
+    def double():
+        state.view().mul_(2)
+
+    desc = sm.RegionDescriptor(name="inplace", accurate_fn=double,
+                               ml=sm.parse_ml_clause(f'ml(collect) inout(state) db("{tmp_path / "db"}")'),
+                               inout_maps=[sm.BoundMap(f, t, state)])
+    with sm.Runtime() as rt:
+        rt.invoke_region(rt.register_region(desc))
+    with sm.open_db(tmp_path / "db", "read") as db:
+        rec = db.read_records("inplace", 0, 1)[0]
+    assert np.array_equal(rec.inputs.to_numpy()[:, 0], np.arange(8))
+    assert np.array_equal(rec.outputs.to_numpy()[:, 0], 2 * np.arange(8))
+
+
+def test_inout_infer_snapshot_semantics(cuda, tmp_path):
+    """in == out buffer: every output computed from the pre-call state."""
+    sm.save_model(sm.Model(1, 1, [sm.DenseLayer(np.array([[2.0]], np.float32), np.array([1.0], np.float32),
+                                                "identity")]), tmp_path / "m")
+    data = np.arange(1000, dtype=np.float32)
+    state = sm.ArrayBuffer.from_numpy(data)
+    f = sm.parse_directive("functor(f: [k, 0:1] = ([k]))")
+    t = sm.parse_directive("map(to: f(state[0:1000]))").targets[0]
+    desc = sm.RegionDescriptor(name="io", accurate_fn=lambda: None,
+                               ml=sm.parse_ml_clause(f'ml(infer) inout(state) model("{tmp_path / "m"}")'),
+                               inout_maps=[sm.BoundMap(f, t, state)])
+    with sm.Runtime() as rt:
+        rt.invoke_region(rt.register_region(desc))
+    assert np.array_equal(state.to_numpy(), data * 2 + 1)
+
+
+def test_nonfinite_checked_commit_leaves_outputs(cuda, tmp_path):
+    sm.save_model(sm.Model(5, 1, [sm.DenseLayer(np.full((1, 5), 1e38, np.float32), np.zeros(1, np.float32),
+                                                "identity")]), tmp_path / "big")
+    for commit in ("checked", "fused"):
+        desc, t, tnew, _ = make_region("infer", model=str(tmp_path / "big"), name=commit)
+        t.view().fill_(10.0)
+        before = tnew.to_numpy()
+        with sm.Runtime(commit=commit) as rt:
+            with pytest.raises(NonFiniteOutputError):
+                rt.invoke_region(rt.register_region(desc))
+        if commit == "checked":
+            assert np.array_equal(tnew.to_numpy(), before)
+
+
+def test_host_buffers_end_to_end(cuda, jdir):
+    """Host-resident ArrayBuffers are staged through HBM (the e2e path)."""
+    f0 = field(3)
+    t = sm.ArrayBuffer(torch.from_numpy(f0.reshape(-1).copy()).pin_memory(), (6, 6), (6, 1))
+    tnew = sm.ArrayBuffer(torch.from_numpy(f0.reshape(-1).copy()), (6, 6), (6, 1))
+    desc = sm.RegionDescriptor(name="host", accurate_fn=lambda: None,
+                               ml=sm.parse_ml_clause(f'ml(infer) in(t) out(tnew) model("{jdir}")'),
+                               in_maps=[sm.BoundMap(IF, TO, t)], out_maps=[sm.BoundMap(OF, FROM, tnew)])
+    with sm.Runtime() as rt:
+        rt.invoke_region(rt.register_region(desc))
+    got = tnew.data.numpy().reshape(6, 6)
+    assert np.array_equal(got[1:-1, 1:-1], jacobi_ref(f0))
+    assert np.array_equal(got[0], f0[0]) and np.array_equal(got[:, 0], f0[:, 0])
+
+
+def test_stats_bounded_by_wall(cuda, jdir):
+    import time
+    desc, *_ = make_region("infer", model=jdir)
+    with sm.Runtime() as rt:
+        h = rt.register_region(desc)
+        t0 = time.perf_counter_ns()
+        for _ in range(5):
+            rt.invoke_region(h)
+        wall = time.perf_counter_ns() - t0
+        st = rt.stats(h)
+    assert st.map_to_ns + st.map_from_ns + st.infer_ns <= wall and st.invocations == 5
