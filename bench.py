@@ -153,7 +153,7 @@ def _inner_rows(wl):
 
 
 # CPU sample per config: about 10-20 s of reference-path work on one core
-CPU_SAMPLE = {"options": 100_000, "bonds": 4_096, "minibude": 256, "miniweather": 64 * 2046}
+CPU_SAMPLE = {"options": 1_000_000, "bonds": 65_536, "minibude": 2_048, "miniweather": 4094 * 2046}
 
 
 def _cpu_sample_elems(name):

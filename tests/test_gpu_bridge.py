@@ -85,7 +85,9 @@ def test_column_major_and_f64_and_round_trip(cuda):
     dst = sm.ArrayBuffer.zeros((6, 5), "f64")
     sm.scatter_from(f, t, x, dst)
     assert np.array_equal(dst.to_numpy()[1:5, 2:4], src.to_numpy()[1:5, 2:4])
-    assert dst.to_numpy().sum() == src.to_numpy()[1:5, 2:4].sum()
+    outside = dst.to_numpy().copy()
+    outside[1:5, 2:4] = 0
+    assert not outside.any()
 
 
 def test_scatter_casts_f32_tensor_into_f64_array(cuda):
