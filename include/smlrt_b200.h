@@ -181,6 +181,11 @@ int smlrt_collect_async(const void* dense_dev, size_t bytes, void* pinned_host,
                         void* side_stream, void* after_event);
 int smlrt_collect_wait(void* side_stream);
 
+/* Diagnostic: one-CTA tcgen05 GEMM D[128 x N] = A[128 x K] * B[N x K]^T
+ * (host f32 in, bf16 operands staged in the fused kernel's SW32/SW128
+ * layouts, f32 out).  Validates descriptor encodings on a new device. */
+int smlrt_tc_selftest(int K, int N, const float* A, const float* B, float* D);
+
 #ifdef __cplusplus
 }
 #endif

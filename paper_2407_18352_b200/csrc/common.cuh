@@ -64,6 +64,8 @@ struct DevPlan {
   const int32_t* col_arr;   // [n_cols] array index
   const int64_t* col_str;   // [n_cols * n_sweep] (non-uniform plans)
   int32_t uarray;           // uniform: the single array index
+  int32_t dense_rows;       // uniform, 1-D sweep, columns one contiguous run
+  int64_t col_off0;         // col_off[0] (host copy, for launch-time decisions)
 };
 
 __host__ __device__ __forceinline__ int64_t row_offset_uniform(const DevPlan& p, uint32_t r) {

@@ -89,6 +89,8 @@ int smlrt_plan_s::tables(DevPlan* p) {
     p->sdiv[k] = FastDiv(k < n_sweep ? (uint32_t)sweep[k] : 1u);
   }
   p->cdiv = FastDiv((uint32_t)n_cols);
+  p->dense_rows = dense_rows;
+  p->col_off0 = col_off.empty() ? 0 : col_off[0];
   p->col_off = it->second.col_off;
   p->col_arr = it->second.col_arr;
   p->col_str = it->second.col_str;
