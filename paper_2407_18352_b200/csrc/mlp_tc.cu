@@ -96,9 +96,53 @@ struct Ptrs8 {
 };
 
 __device__ __forceinline__ float act_f(float y, int act) {
-  if (act == SMLRT_RELU) return (y < 0.0f) ? 0.0f : y;
+  if (act == SMLRT_RELU) return relu_nan(y);
   if (act == SMLRT_TANH) return tanhf(y);
   return y;
+}
+
+template <int ACT>
+__device__ __forceinline__ float act_t(float y) {
+  if constexpr (ACT == SMLRT_RELU) return relu_nan(y);
+  else if constexpr (ACT == SMLRT_TANH) return tanhf(y);
+  else return y;
+}
+
+template <int ACT>
+__device__ __forceinline__ uint32_t act_pack(float lo, float hi) {
+  if constexpr (ACT == SMLRT_RELU) return pack_relu_bf16(lo, hi);
+  else return pack_bf16(act_t<ACT>(lo), act_t<ACT>(hi));
+}
+
+// epilogue 1 for one 32-column slab: +b1, activation, bf16, SW128 st.shared
+template <int ACT>
+__device__ __forceinline__ void epi1_slab(const uint32_t (&v)[32], const float* b1, int c0, uint32_t a2,
+                                          int a2_chunk, int r) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + 8 * j;
+    const float4 bl = *reinterpret_cast<const float4*>(b1 + c);
+    const float4 bh = *reinterpret_cast<const float4*>(b1 + c + 4);
+    const float* x = reinterpret_cast<const float*>(v) + 8 * j;
+    st_shared_v4(a2 + (c >> 6) * a2_chunk + sw128_offset(r, c & 63),
+                 act_pack<ACT>(x[0] + bl.x, x[1] + bl.y), act_pack<ACT>(x[2] + bl.z, x[3] + bl.w),
+                 act_pack<ACT>(x[4] + bh.x, x[5] + bh.y), act_pack<ACT>(x[6] + bh.z, x[7] + bh.w));
+  }
+}
+
+// epilogue 2 for one 32-column slab: acc += act(v + b2) * w3
+template <int ACT>
+__device__ __forceinline__ void epi2_slab(const uint32_t (&v)[32], const float* b2, const float* w3, int c0,
+                                          float (&acc)[4]) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 4) {
+    const float4 bb = *reinterpret_cast<const float4*>(b2 + c0 + e);
+    const float4 ww = *reinterpret_cast<const float4*>(w3 + c0 + e);
+    acc[0] = fmaf(act_t<ACT>(__uint_as_float(v[e]) + bb.x), ww.x, acc[0]);
+    acc[1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1]) + bb.y), ww.y, acc[1]);
+    acc[2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2]) + bb.z), ww.z, acc[2]);
+    acc[3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3]) + bb.w), ww.w, acc[3]);
+  }
 }
 
 __device__ __forceinline__ float ld_elem(const void* base, int dt, int64_t i) {
@@ -267,15 +311,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tc_fence_before();
           mbar_arrive(bar + L::B_L1EMPTY);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c = c0 + 8 * j;
-          float f[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) f[e] = act_f(__uint_as_float(v[8 * j + e]) + b1[c + e], a.act1);
-          st_shared_v4(a2 + (c >> 6) * L::A2_CHUNK + sw128_offset(r, c & 63), pack_bf16(f[0], f[1]),
-                       pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
-        }
+        if (a.act1 == SMLRT_RELU)
+          epi1_slab<SMLRT_RELU>(v, b1, c0, a2, L::A2_CHUNK, r);
+        else if (a.act1 == SMLRT_TANH)
+          epi1_slab<SMLRT_TANH>(v, b1, c0, a2, L::A2_CHUNK, r);
+        else
+          epi1_slab<SMLRT_IDENTITY>(v, b1, c0, a2, L::A2_CHUNK, r);
       }
       fence_async_smem();
       mbar_arrive(bar + L::B_A2FULL + b);
@@ -298,11 +339,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t v[32];
         tmem_ld32(lane_addr + L::T_L2 + b * H2 + cc * 32, v);
         tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int c = cc * 32 + e;
-          acc[e & 3] = fmaf(act_f(__uint_as_float(v[e]) + b2[c], a.act2), w3[c], acc[e & 3]);
-        }
+        if (a.act2 == SMLRT_RELU)
+          epi2_slab<SMLRT_RELU>(v, b2, w3, cc * 32, acc);
+        else if (a.act2 == SMLRT_TANH)
+          epi2_slab<SMLRT_TANH>(v, b2, w3, cc * 32, acc);
+        else
+          epi2_slab<SMLRT_IDENTITY>(v, b2, w3, cc * 32, acc);
       }
       tc_fence_before();
       mbar_arrive(bar + L::B_L2EMPTY + b);

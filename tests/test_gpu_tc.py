@@ -111,3 +111,18 @@ def test_bonds_full_size_properties(cuda, tmp_path):
         with sm.Runtime(shard=(r, 4)) as rt:
             rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "m"))))
     assert torch.equal(first, wl.buffers["val"].data)
+
+
+def test_bf16_relu_propagates_nan(cuda, tmp_path):
+    """np.maximum semantics: a NaN input must surface as NonFiniteOutputError
+    through both bf16 relu epilogues (cvt.relu and max.NaN)."""
+    from paper_2407_18352_b200.errors import NonFiniteOutputError
+    wl = workloads.make("bonds", 4096)
+    wl.arrays["bonds"][1234, 3] = np.nan
+    wl.to_device()
+    sm.save_model(wl.model, tmp_path / "m")
+    with sm.Runtime() as rt:
+        with pytest.raises(NonFiniteOutputError):
+            rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "m"))))
+    got = wl.buffers["val"].to_numpy()
+    assert np.isnan(got[1234]) and np.isfinite(np.delete(got, 1234)).all()
