@@ -33,10 +33,14 @@ using namespace ptx;
 
 constexpr int BM = 128;
 constexpr int KX = 16;
-constexpr int XSTAGES = 4;
+constexpr int XSTAGES = 2;
 constexpr int WARP_EPI2 = 0, WARP_EPI1 = 4, WARP_LOAD = 12, WARP_MMA = 16;
 constexpr int NTHREADS = 17 * 32;
 
+// Biases ride on the tensor cores: a constant "ones" tile [128 x 16] (columns
+// 0 and 1 = 1.0) times a bias tile [N x 16] holding bf16(b) in k=0 and
+// bf16(b - bf16(b)) in k=1 adds b (to ~16 mantissa bits) to every row of the
+// accumulator, so the epilogues never touch the biases.
 template <int H1, int H2>
 struct Lay {
   static_assert(H1 % 64 == 0 && H1 >= 64 && H1 <= 256, "H1: multiple of 64, <= 256");
@@ -49,11 +53,12 @@ struct Lay {
   static constexpr int X_STAGE = BM * 32;     // [128][16] bf16, SW32
   static constexpr int OFF_W2 = 0;
   static constexpr int OFF_A2 = OFF_W2 + KC * W2_CHUNK;
-  static constexpr int OFF_W1 = OFF_A2 + 2 * A2_BUF;
-  static constexpr int OFF_X = OFF_W1 + H1 * 32;
-  static constexpr int OFF_B1 = OFF_X + XSTAGES * X_STAGE;
-  static constexpr int OFF_B2 = OFF_B1 + H1 * 4;
-  static constexpr int OFF_W3 = OFF_B2 + H2 * 4;
+  static constexpr int OFF_W1 = OFF_A2 + 2 * A2_BUF;   // [H1][16] SW32
+  static constexpr int OFF_W1B = OFF_W1 + H1 * 32;     // [H1][16] SW32 bias tile
+  static constexpr int OFF_W2B = OFF_W1B + H1 * 32;    // [H2][16] SW32 bias tile
+  static constexpr int OFF_ONES = OFF_W2B + H2 * 32;   // [128][16] SW32
+  static constexpr int OFF_X = OFF_ONES + BM * 32;
+  static constexpr int OFF_W3 = OFF_X + XSTAGES * X_STAGE;
   static constexpr int OFF_B3 = OFF_W3 + H2 * 4;
   static constexpr int OFF_BAR = OFF_B3 + 16;
   enum {
@@ -70,18 +75,18 @@ struct Lay {
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int BYTES = OFF_TMEM + 16;
   static constexpr int ALLOC = BYTES + 1024;  // 1 KB alignment slack (SW128 atoms)
-  // global blob produced by tc_pack_model: W2 img | W1 img | b1 | b2 | w3 | b3
+  static_assert(ALLOC <= 232448, "shared memory budget");
+  // global blob produced by tc_pack_model: W2 | W1 | W1B | W2B | w3 | b3 (same order as smem)
   static constexpr int BLOB_W1 = KC * W2_CHUNK;
-  static constexpr int BLOB_TAIL = BLOB_W1 + H1 * 32;
-  static constexpr int TAIL = H1 * 4 + 2 * H2 * 4 + 16;
+  static constexpr int BLOB_TAIL = BLOB_W1 + 2 * H1 * 32 + H2 * 32;
+  static constexpr int TAIL = H2 * 4 + 16;
   static constexpr int BLOB = BLOB_TAIL + TAIL;
   static constexpr int T_L1 = 0, T_L2 = H1;  // TMEM column bases
 };
 
 struct TcArgs {
   const uint8_t* blob;
-  const float* x_fast;  // dense f32 rows of 16 (fast gather path) or nullptr
-  int64_t x_pitch;      // elements between rows on the fast path
+  const float* x_fast;  // dense contiguous f32 rows of 16 (fast gather path) or nullptr
   int F;
   int act1, act2, act3;
   int64_t r0, r1;
@@ -114,40 +119,124 @@ __device__ __forceinline__ uint32_t act_pack(float lo, float hi) {
   else return pack_bf16(act_t<ACT>(lo), act_t<ACT>(hi));
 }
 
-// epilogue 1 for one 32-column slab: +b1, activation, bf16, SW128 st.shared
-template <int ACT>
-__device__ __forceinline__ void epi1_slab(const uint32_t (&v)[32], const float* b1, int c0, uint32_t a2,
-                                          int a2_chunk, int r) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int c = c0 + 8 * j;
-    const float4 bl = *reinterpret_cast<const float4*>(b1 + c);
-    const float4 bh = *reinterpret_cast<const float4*>(b1 + c + 4);
-    const float* x = reinterpret_cast<const float*>(v) + 8 * j;
-    st_shared_v4(a2 + (c >> 6) * a2_chunk + sw128_offset(r, c & 63),
-                 act_pack<ACT>(x[0] + bl.x, x[1] + bl.y), act_pack<ACT>(x[2] + bl.z, x[3] + bl.w),
-                 act_pack<ACT>(x[4] + bh.x, x[5] + bh.y), act_pack<ACT>(x[6] + bh.z, x[7] + bh.w));
-  }
-}
-
-// epilogue 2 for one 32-column slab: acc += act(v + b2) * w3
-template <int ACT>
-__device__ __forceinline__ void epi2_slab(const uint32_t (&v)[32], const float* b2, const float* w3, int c0,
-                                          float (&acc)[4]) {
-#pragma unroll
-  for (int e = 0; e < 32; e += 4) {
-    const float4 bb = *reinterpret_cast<const float4*>(b2 + c0 + e);
-    const float4 ww = *reinterpret_cast<const float4*>(w3 + c0 + e);
-    acc[0] = fmaf(act_t<ACT>(__uint_as_float(v[e]) + bb.x), ww.x, acc[0]);
-    acc[1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1]) + bb.y), ww.y, acc[1]);
-    acc[2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2]) + bb.z), ww.z, acc[2]);
-    acc[3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3]) + bb.w), ww.w, acc[3]);
-  }
-}
-
 __device__ __forceinline__ float ld_elem(const void* base, int dt, int64_t i) {
   return dt == SMLRT_F32 ? __ldg(reinterpret_cast<const float*>(base) + i)
                          : __double2float_rn(__ldg(reinterpret_cast<const double*>(base) + i));
+}
+
+// ------------------------------------------------------------ epilogue 1
+// TMEM L1 accumulator (bias already added by the MMA) -> act -> bf16 ->
+// A2[b] in the SW128 K-major layout layer 2 consumes.  Thread = row r; this
+// warpgroup covers columns [half*H1/2, (half+1)*H1/2).
+template <int ACT, int H1, int H2>
+__device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int half,
+                                          int q, int lane) {
+  using L = Lay<H1, H2>;
+  constexpr int HC = H1 / 2;
+  const int r = q * 32 + lane;
+  const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L1 + half * HC;
+  // swizzled 16-B chunk j of row r lives at rowbase + ((j ^ (r&7)) << 4)
+  const uint32_t rowbase = smem_u32(smem + L::OFF_A2) + r * 128 + (half * HC / 64) * L::A2_CHUNK;
+  uint32_t xo[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) xo[j] = rowbase + ((j ^ (r & 7)) << 4);
+  for (int it = 0; it < n_my; ++it) {
+    const int b = it & 1;
+    mbar_wait(bar + L::B_L1FULL, it & 1);
+    mbar_wait(bar + L::B_A2EMPTY + b, ((it >> 1) & 1) ^ 1);
+    tc_fence_after();
+    const uint32_t boff = b * L::A2_BUF;
+#pragma unroll
+    for (int cc = 0; cc < HC / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(lane_addr + cc * 32, v);
+      tmem_wait_ld();
+      if (cc == HC / 32 - 1) {
+        tc_fence_before();
+        mbar_arrive(bar + L::B_L1EMPTY);
+      }
+      const float* f = reinterpret_cast<const float*>(v);
+      const uint32_t coff = boff + (cc >> 1) * L::A2_CHUNK;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st_shared_v4(xo[(cc & 1) * 4 + j] + coff, act_pack<ACT>(f[8 * j], f[8 * j + 1]),
+                     act_pack<ACT>(f[8 * j + 2], f[8 * j + 3]), act_pack<ACT>(f[8 * j + 4], f[8 * j + 5]),
+                     act_pack<ACT>(f[8 * j + 6], f[8 * j + 7]));
+    }
+    fence_async_smem();
+    mbar_arrive(bar + L::B_A2FULL + b);
+  }
+}
+
+// ------------------------------------------------------------ epilogue 2
+// TMEM L2 accumulator (+b2 from the MMA) -> act -> dot w3 -> +b3 -> act3 ->
+// scatter.  Thread = row.
+template <int ACT, int H1, int H2>
+__device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int q, int lane,
+                                          const TcArgs& a, const DevPlan& Pout, const Ptrs8& dst) {
+  using L = Lay<H1, H2>;
+  const int r = q * 32 + lane;
+  const uint32_t w3 = smem_u32(smem + L::OFF_W3);
+  const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
+  const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L2;
+  const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 && a.staged == nullptr;
+  float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
+                             : nullptr;
+  for (int it = 0; it < n_my; ++it) {
+    const int b = it & 1;
+    mbar_wait(bar + L::B_L2FULL + b, (it >> 1) & 1);
+    tc_fence_after();
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int cc = 0; cc < H2 / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(lane_addr + b * H2 + cc * 32, v);
+      tmem_wait_ld();
+      if (cc == H2 / 32 - 1) {
+        tc_fence_before();
+        mbar_arrive(bar + L::B_L2EMPTY + b);
+      }
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        const float4 ww = ld_shared_f4(w3 + (cc * 32 + e) * 4);
+        acc[((e >> 2) & 1) * 4 + 0] = fmaf(act_t<ACT>(__uint_as_float(v[e])), ww.x, acc[((e >> 2) & 1) * 4 + 0]);
+        acc[((e >> 2) & 1) * 4 + 1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1])), ww.y, acc[((e >> 2) & 1) * 4 + 1]);
+        acc[((e >> 2) & 1) * 4 + 2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2])), ww.z, acc[((e >> 2) & 1) * 4 + 2]);
+        acc[((e >> 2) & 1) * 4 + 3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3])), ww.w, acc[((e >> 2) & 1) * 4 + 3]);
+      }
+    }
+    const float y = act_f(((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + b3,
+                          a.act3);
+    const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+    const int64_t row = a.r0 + tile * BM + r;
+    bool bad = false;
+    if (row < a.r1) {
+      bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
+      if (out_fast) {
+        out_base[row * Pout.ustride[0]] = y;
+      } else if (a.staged != nullptr) {
+        a.staged[row - a.r0] = y;
+      } else {
+        int64_t addr;
+        int arr;
+        if (Pout.uniform) {
+          addr = Pout.col_off0 + row_offset_uniform(Pout, (uint32_t)row);
+          arr = Pout.uarray;
+        } else {
+          uint32_t idx[SMLRT_MAX_SWEEP];
+          unravel(Pout, (uint32_t)row, idx);
+          addr = col_address(Pout, 0, idx);
+          arr = __ldg(Pout.col_arr);
+        }
+        void* base = const_cast<void*>(dst.p[arr]);
+        if (dst.dt[arr] == SMLRT_F32)
+          reinterpret_cast<float*>(base)[addr] = y;
+        else
+          reinterpret_cast<double*>(base)[addr] = (double)y;
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+  }
 }
 
 template <int H1, int H2>
@@ -179,14 +268,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_fence_init();
   }
   if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
-  {  // resident weights: blob -> smem (16-byte vectors)
+  {  // resident weights: blob -> smem (16-byte vectors); ones tile built here
     const int4* g = reinterpret_cast<const int4*>(a.blob);
     for (int i = threadIdx.x; i < L::BLOB_W1 / 16; i += NTHREADS)
       reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
-    for (int i = threadIdx.x; i < H1 * 32 / 16; i += NTHREADS)
+    for (int i = threadIdx.x; i < (L::BLOB_TAIL - L::BLOB_W1) / 16; i += NTHREADS)
       reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[L::BLOB_W1 / 16 + i];
     for (int i = threadIdx.x; i < L::TAIL / 16; i += NTHREADS)
-      reinterpret_cast<int4*>(smem + L::OFF_B1)[i] = g[L::BLOB_TAIL / 16 + i];
+      reinterpret_cast<int4*>(smem + L::OFF_W3)[i] = g[L::BLOB_TAIL / 16 + i];
+    for (int i = threadIdx.x; i < BM * KX; i += NTHREADS) {
+      const int row = i / KX, k = i % KX;
+      *reinterpret_cast<__nv_bfloat16*>(smem + L::OFF_ONES + sw32_offset(row, k)) =
+          __float2bfloat16_rn(k < 2 ? 1.0f : 0.0f);
+    }
   }
   fence_async_smem();
   tc_fence_before();
@@ -197,89 +291,119 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (warp >= WARP_LOAD && warp < WARP_MMA) {
     // ============================================================ loader
-    const int t = threadIdx.x - WARP_LOAD * 32;  // tile row
-    float cur[16], nxt[16];
-    auto load_row = [&](int it, float(&v)[16]) {
-      const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-      const int64_t row = a.r0 + tile * BM + t;
+    const int t = threadIdx.x - WARP_LOAD * 32;
+    const uint32_t xbase = smem_u32(smem + L::OFF_X);
+    if (a.x_fast != nullptr) {
+      // tile = 2048 contiguous floats: thread t moves float4 #(t + 128 i), i < 4
+      float4 cur[4], nxt[4];
+      auto load_tile = [&](int it, float4(&v)[4]) {
+        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+        const int64_t row0 = a.r0 + tile * BM;
 #pragma unroll
-      for (int f = 0; f < 16; ++f) v[f] = 0.0f;
-      if (row >= a.r1) return;
-      if (a.x_fast != nullptr) {
-        const float4* p = reinterpret_cast<const float4*>(a.x_fast + row * a.x_pitch);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float4 u = __ldg(p + q);
-          v[4 * q] = u.x;
-          v[4 * q + 1] = u.y;
-          v[4 * q + 2] = u.z;
-          v[4 * q + 3] = u.w;
+        for (int i = 0; i < 4; ++i) {
+          const int idx = t + 128 * i;
+          const int64_t row = row0 + (idx >> 2);
+          v[i] = row < a.r1 ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-      } else if (Pin.uniform) {
-        const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
-        const void* base = src.p[Pin.uarray];
-        const int dt = src.dt[Pin.uarray];
+      };
+      if (n_my > 0) load_tile(0, cur);
+      for (int it = 0; it < n_my; ++it) {
+        if (it + 1 < n_my) load_tile(it + 1, nxt);
+        const int s = it % XSTAGES;
+        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
+        const uint32_t xs = xbase + s * L::X_STAGE;
 #pragma unroll
-        for (int f = 0; f < 16; ++f)
-          if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
-      } else {
-        uint32_t idx[SMLRT_MAX_SWEEP];
-        unravel(Pin, (uint32_t)row, idx);
+        for (int i = 0; i < 4; ++i) {
+          const int idx = t + 128 * i;
+          st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(cur[i].x, cur[i].y),
+                       pack_bf16(cur[i].z, cur[i].w));
+        }
+        fence_async_smem();
+        mbar_arrive(bar + L::B_XFULL + s);
 #pragma unroll
-        for (int f = 0; f < 16; ++f)
-          if (f < a.F) {
-            const int arr = __ldg(Pin.col_arr + f);
-            v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
-          }
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       }
-    };
-    if (n_my > 0) load_row(0, cur);
-    for (int it = 0; it < n_my; ++it) {
-      if (it + 1 < n_my) load_row(it + 1, nxt);
-      const int s = it % XSTAGES;
-      mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-      const uint32_t xs = smem_u32(smem + L::OFF_X + s * L::X_STAGE);
-      st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
-                   pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
-      st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
-                   pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
-      fence_async_smem();
-      mbar_arrive(bar + L::B_XFULL + s);
+    } else {
+      // general plan-driven gather: thread = tile row
+      float cur[16], nxt[16];
+      auto load_row = [&](int it, float(&v)[16]) {
+        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+        const int64_t row = a.r0 + tile * BM + t;
 #pragma unroll
-      for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
+        for (int f = 0; f < 16; ++f) v[f] = 0.0f;
+        if (row >= a.r1) return;
+        if (Pin.uniform) {
+          const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
+          const void* base = src.p[Pin.uarray];
+          const int dt = src.dt[Pin.uarray];
+#pragma unroll
+          for (int f = 0; f < 16; ++f)
+            if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
+        } else {
+          uint32_t idx[SMLRT_MAX_SWEEP];
+          unravel(Pin, (uint32_t)row, idx);
+#pragma unroll
+          for (int f = 0; f < 16; ++f)
+            if (f < a.F) {
+              const int arr = __ldg(Pin.col_arr + f);
+              v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
+            }
+        }
+      };
+      if (n_my > 0) load_row(0, cur);
+      for (int it = 0; it < n_my; ++it) {
+        if (it + 1 < n_my) load_row(it + 1, nxt);
+        const int s = it % XSTAGES;
+        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
+        const uint32_t xs = xbase + s * L::X_STAGE;
+        st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
+                     pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
+        st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
+                     pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
+        fence_async_smem();
+        mbar_arrive(bar + L::B_XFULL + s);
+#pragma unroll
+        for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
+      }
     }
   } else if (warp == WARP_MMA) {
     // ========================================================= MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc1 = idesc_bf16(BM, H1);
       constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
-      const uint32_t w1 = smem_u32(smem + L::OFF_W1);
       const uint32_t w2 = smem_u32(smem + L::OFF_W2);
       const uint32_t x0 = smem_u32(smem + L::OFF_X);
       const uint32_t a20 = smem_u32(smem + L::OFF_A2);
+      const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
+      const uint64_t w1bd = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
+      const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
+      const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
       auto issue_l2 = [&](int j) {
         const int b = j & 1;
         mbar_wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
         mbar_wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
         tc_fence_after();
+        const uint32_t d = tbase + L::T_L2 + b * H2;
+        mma_bf16(d, onesd, w2bd, idesc2, 0);  // D = b2
 #pragma unroll
         for (int kc = 0; kc < L::KC; ++kc)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = smem_desc(a20 + b * L::A2_BUF + kc * L::A2_CHUNK + k * 32, 1024, kSwizzle128);
             const uint64_t bd = smem_desc(w2 + kc * L::W2_CHUNK + k * 32, 1024, kSwizzle128);
-            mma_bf16(tbase + L::T_L2 + b * H2, ad, bd, idesc2, (kc | k) != 0);
+            mma_bf16(d, ad, bd, idesc2, 1);
           }
         mma_commit(bar + L::B_A2EMPTY + b);
         mma_commit(bar + L::B_L2FULL + b);
       };
-      const uint64_t w1d = smem_desc(w1, 256, kSwizzle32);
       for (int it = 0; it < n_my; ++it) {
         const int s = it % XSTAGES;
         mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
         mbar_wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
         tc_fence_after();
-        mma_bf16(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, 0);
+        mma_bf16(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1
+        mma_bf16(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, 1);
         mma_commit(bar + L::B_XEMPTY + s);
         mma_commit(bar + L::B_L1FULL);
         if (it > 0) issue_l2(it - 1);
@@ -288,95 +412,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp >= WARP_EPI1) {
-    // ======================================================== epilogue 1
     const int half = (warp - WARP_EPI1) >> 2;
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    constexpr int HC = H1 / 2;
-    const float* b1 = reinterpret_cast<const float*>(smem + L::OFF_B1);
-    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
-    for (int it = 0; it < n_my; ++it) {
-      const int b = it & 1;
-      mbar_wait(bar + L::B_L1FULL, it & 1);
-      mbar_wait(bar + L::B_A2EMPTY + b, ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t a2 = smem_u32(smem + L::OFF_A2 + b * L::A2_BUF);
-#pragma unroll 1
-      for (int cc = 0; cc < HC / 32; ++cc) {
-        const int c0 = half * HC + cc * 32;
-        uint32_t v[32];
-        tmem_ld32(lane_addr + L::T_L1 + c0, v);
-        tmem_wait_ld();
-        if (cc == HC / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(bar + L::B_L1EMPTY);
-        }
-        if (a.act1 == SMLRT_RELU)
-          epi1_slab<SMLRT_RELU>(v, b1, c0, a2, L::A2_CHUNK, r);
-        else if (a.act1 == SMLRT_TANH)
-          epi1_slab<SMLRT_TANH>(v, b1, c0, a2, L::A2_CHUNK, r);
-        else
-          epi1_slab<SMLRT_IDENTITY>(v, b1, c0, a2, L::A2_CHUNK, r);
-      }
-      fence_async_smem();
-      mbar_arrive(bar + L::B_A2FULL + b);
-    }
+    if (a.act1 == SMLRT_RELU)
+      epilogue1<SMLRT_RELU, H1, H2>(smem, bar, tbase, n_my, half, warp & 3, lane);
+    else if (a.act1 == SMLRT_TANH)
+      epilogue1<SMLRT_TANH, H1, H2>(smem, bar, tbase, n_my, half, warp & 3, lane);
+    else
+      epilogue1<SMLRT_IDENTITY, H1, H2>(smem, bar, tbase, n_my, half, warp & 3, lane);
   } else {
-    // ======================================================== epilogue 2
-    const int q = warp;  // warps 0-3
-    const int r = q * 32 + lane;
-    const float* b2 = reinterpret_cast<const float*>(smem + L::OFF_B2);
-    const float* w3 = reinterpret_cast<const float*>(smem + L::OFF_W3);
-    const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
-    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
-    for (int it = 0; it < n_my; ++it) {
-      const int b = it & 1;
-      mbar_wait(bar + L::B_L2FULL + b, (it >> 1) & 1);
-      tc_fence_after();
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-      for (int cc = 0; cc < H2 / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(lane_addr + L::T_L2 + b * H2 + cc * 32, v);
-        tmem_wait_ld();
-        if (a.act2 == SMLRT_RELU)
-          epi2_slab<SMLRT_RELU>(v, b2, w3, cc * 32, acc);
-        else if (a.act2 == SMLRT_TANH)
-          epi2_slab<SMLRT_TANH>(v, b2, w3, cc * 32, acc);
-        else
-          epi2_slab<SMLRT_IDENTITY>(v, b2, w3, cc * 32, acc);
-      }
-      tc_fence_before();
-      mbar_arrive(bar + L::B_L2EMPTY + b);
-      const float y = act_f((acc[0] + acc[1]) + (acc[2] + acc[3]) + b3, a.act3);
-      const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-      const int64_t row = a.r0 + tile * BM + r;
-      bool bad = false;
-      if (row < a.r1) {
-        bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
-        if (a.staged != nullptr) {
-          a.staged[row - a.r0] = y;
-        } else {
-          int64_t addr;
-          int arr;
-          if (Pout.uniform) {
-            addr = __ldg(Pout.col_off) + row_offset_uniform(Pout, (uint32_t)row);
-            arr = Pout.uarray;
-          } else {
-            uint32_t idx[SMLRT_MAX_SWEEP];
-            unravel(Pout, (uint32_t)row, idx);
-            addr = col_address(Pout, 0, idx);
-            arr = __ldg(Pout.col_arr);
-          }
-          void* base = const_cast<void*>(dst.p[arr]);
-          if (dst.dt[arr] == SMLRT_F32)
-            reinterpret_cast<float*>(base)[addr] = y;
-          else
-            reinterpret_cast<double*>(base)[addr] = (double)y;
-        }
-      }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
-    }
+    if (a.act2 == SMLRT_RELU)
+      epilogue2<SMLRT_RELU, H1, H2>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst);
+    else if (a.act2 == SMLRT_TANH)
+      epilogue2<SMLRT_TANH, H1, H2>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst);
+    else
+      epilogue2<SMLRT_IDENTITY, H1, H2>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst);
   }
 
   // -------------------------------------------------------------- teardown
@@ -412,16 +461,28 @@ std::vector<uint8_t> pack(const smlrt_model_s& m) {
     uint16_t h = f2bf(v);
     std::memcpy(blob.data() + off, &h, 2);
   };
+  auto bf = [](float v) {  // value of the bf16 rounding of v
+    uint32_t u = (uint32_t)f2bf(v) << 16;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+  };
   for (int kc = 0; kc < L::KC; ++kc)
     for (int n = 0; n < H2; ++n)
       for (int k = 0; k < 64; ++k) put(kc * L::W2_CHUNK + sw128_offset(n, k), W2[(size_t)n * H1 + kc * 64 + k]);
-  for (int n = 0; n < H1; ++n)
-    for (int k = 0; k < KX; ++k) put(L::BLOB_W1 + sw32_offset(n, k), k < F ? W1[(size_t)n * F + k] : 0.0f);
+  const size_t o_w1 = L::BLOB_W1, o_w1b = o_w1 + H1 * 32, o_w2b = o_w1b + H1 * 32;
+  for (int n = 0; n < H1; ++n) {
+    for (int k = 0; k < KX; ++k) put(o_w1 + sw32_offset(n, k), k < F ? W1[(size_t)n * F + k] : 0.0f);
+    put(o_w1b + sw32_offset(n, 0), b1[n]);
+    put(o_w1b + sw32_offset(n, 1), b1[n] - bf(b1[n]));
+  }
+  for (int n = 0; n < H2; ++n) {
+    put(o_w2b + sw32_offset(n, 0), b2[n]);
+    put(o_w2b + sw32_offset(n, 1), b2[n] - bf(b2[n]));
+  }
   float* tail = reinterpret_cast<float*>(blob.data() + L::BLOB_TAIL);
-  std::memcpy(tail, b1, H1 * 4);
-  std::memcpy(tail + H1, b2, H2 * 4);
-  std::memcpy(tail + H1 + H2, W3, H2 * 4);
-  tail[H1 + 2 * H2] = b3[0];
+  std::memcpy(tail, W3, H2 * 4);
+  tail[H2] = b3[0];
   return blob;
 }
 
@@ -470,13 +531,11 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     dst.p[i] = out_ptrs[i];
     dst.dt[i] = out_dt[i];
   }
-  // fast gather: one f32 array, 16 contiguous features per row, 16-B aligned
-  if (in.dense_rows && in.n_cols == 16 && m.in_features == 16 && in_dt[in.uarray] == SMLRT_F32) {
+  // fast gather: one f32 array of dense 16-float rows (a contiguous tile), 16-B aligned
+  if (in.dense_rows && in.n_cols == 16 && in.ustride[0] == 16 && m.in_features == 16 &&
+      in_dt[in.uarray] == SMLRT_F32) {
     const float* base = reinterpret_cast<const float*>(in_ptrs[in.uarray]) + in.col_off0;
-    if (in.ustride[0] % 4 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0) {
-      a.x_fast = base;
-      a.x_pitch = in.ustride[0];
-    }
+    if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
   const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
   mlp3_tc_kernel<H1, H2><<<grid, NTHREADS, L::ALLOC, s>>>(a, in, src, out, dst);
