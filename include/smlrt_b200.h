@@ -185,6 +185,8 @@ int smlrt_collect_wait(void* side_stream);
  * (host f32 in, bf16 operands staged in the fused kernel's SW32/SW128
  * layouts, f32 out).  Validates descriptor encodings on a new device. */
 int smlrt_tc_selftest(int K, int N, const float* A, const float* B, float* D);
+/* Same with A staged in TMEM by tcgen05.st (the TS operand path). */
+int smlrt_tc_selftest_ts(int K, int N, const float* A, const float* B, float* D);
 
 #ifdef __cplusplus
 }

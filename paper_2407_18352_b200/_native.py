@@ -84,6 +84,7 @@ SIGNATURES = {
     "smlrt_collect_async": (_I, [_P, C.c_size_t, _P, _P, _P]),
     "smlrt_collect_wait": (_I, [_P]),
     "smlrt_tc_selftest": (_I, [_I, _I, _P, _P, _P]),
+    "smlrt_tc_selftest_ts": (_I, [_I, _I, _P, _P, _P]),
 }
 
 _lib = None
@@ -245,11 +246,13 @@ def collect_wait(side_stream):
     _check(lib().smlrt_collect_wait(side_stream))
 
 
-def tc_selftest(A, B):
-    """D = A @ B.T on one CTA through tcgen05 (A [128,K], B [N,K] float32)."""
+def tc_selftest(A, B, tmem_a: bool = False):
+    """D = A @ B.T on one CTA through tcgen05 (A [128,K], B [N,K] float32);
+    tmem_a stages A in tensor memory (TS form) instead of shared memory."""
     import numpy as np
     A = np.ascontiguousarray(A, np.float32)
     B = np.ascontiguousarray(B, np.float32)
     D = np.zeros((128, B.shape[0]), np.float32)
-    _check(lib().smlrt_tc_selftest(A.shape[1], B.shape[0], A.ctypes.data, B.ctypes.data, D.ctypes.data))
+    fn = lib().smlrt_tc_selftest_ts if tmem_a else lib().smlrt_tc_selftest
+    _check(fn(A.shape[1], B.shape[0], A.ctypes.data, B.ctypes.data, D.ctypes.data))
     return D

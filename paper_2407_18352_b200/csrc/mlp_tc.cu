@@ -437,6 +437,404 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ============================================================================
+// v2: layer-2 A operand from TMEM ("TS" MMA), layer 1 streamed in 64-feature
+// chunks.  Per chunk g (tile i = g / NCH, chunk c = g % NCH):
+//   MMA   L1c : S[g&1] = ones*W1B_c + X_i*W1_c          (M=128, N=64, SMEM operands)
+//   epi1      : S[g&1] -> act -> bf16 pairs -> tcgen05.st -> R[g&1]   (no SMEM)
+//   MMA   L2c : D[i&1] (+)= R[g&1] * W2_c  (4 x K=16, A from TMEM); c==0 adds ones*W2B
+//   epi2      : D[i&1] -> act -> dot w3 -> +b3 -> scatter
+// TMEM: S 2x64 + R 2x32 + D 2xH2 <= 512 columns.  SMEM holds only weights,
+// the ones tile and the X ring, and the tensor core reads only the B operand
+// (weights) from it for layer 2 -- the operand stream that saturated the
+// SMEM port in v1 (A2 reads + the epilogue's A2 writes) is gone.
+constexpr int CH = 64;
+
+template <int H1, int H2>
+struct LayTS {
+  static_assert(H1 % CH == 0 && H1 >= CH && H1 <= 256, "H1: multiple of 64, <= 256");
+  static_assert(H2 % 32 == 0 && H2 >= 32 && 4 * CH + 2 * H2 <= 512, "H2 <= 128 (TMEM)");
+  static constexpr int NCH = H1 / CH;
+  static constexpr int W2_CHUNK = H2 * 128;  // [H2][64] bf16 SW128 (K chunk c of W2)
+  static constexpr int W1_CHUNK = CH * 32;   // [64][16] bf16 SW32 (rows 64c.. of W1)
+  static constexpr int X_STAGE = BM * 32;
+  static constexpr int XS = 4;
+  static constexpr int OFF_W2 = 0;
+  static constexpr int OFF_W1 = OFF_W2 + NCH * W2_CHUNK;
+  static constexpr int OFF_W1B = OFF_W1 + H1 * 32;
+  static constexpr int OFF_W2B = OFF_W1B + H1 * 32;
+  static constexpr int OFF_ONES = OFF_W2B + H2 * 32;
+  static constexpr int OFF_X = OFF_ONES + BM * 32;
+  static constexpr int OFF_W3 = OFF_X + XS * X_STAGE;
+  static constexpr int OFF_B3 = OFF_W3 + H2 * 4;
+  static constexpr int OFF_BAR = OFF_B3 + 16;
+  enum {
+    B_XFULL = 0,
+    B_XEMPTY = XS,
+    B_SFULL = 2 * XS,
+    B_SEMPTY = B_SFULL + 2,
+    B_RFULL = B_SEMPTY + 2,
+    B_REMPTY = B_RFULL + 2,
+    B_DFULL = B_REMPTY + 2,
+    B_DEMPTY = B_DFULL + 2,
+    N_BAR = B_DEMPTY + 2
+  };
+  static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
+  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
+  static_assert(ALLOC <= 232448, "shared memory budget");
+  // blob (same layout as v1's pack): W2 | W1 | W1B | W2B | w3 | b3
+  static constexpr int BLOB_W1 = NCH * W2_CHUNK;
+  static constexpr int BLOB_TAIL = BLOB_W1 + 2 * H1 * 32 + H2 * 32;
+  static constexpr int TAIL = H2 * 4 + 16;
+  static constexpr int T_S = 0, T_R = 2 * CH, T_D = 3 * CH + CH;  // D at column 256
+};
+
+template <int H1, int H2>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    mlp3_ts_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
+                   const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
+                   const __grid_constant__ Ptrs8 dst) {
+  using L = LayTS<H1, H2>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::XS; ++s) {
+      mbar_init(bar + L::B_XFULL + s, 128);
+      mbar_init(bar + L::B_XEMPTY + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar + L::B_SFULL + b, 1);
+      mbar_init(bar + L::B_SEMPTY + b, 256);
+      mbar_init(bar + L::B_RFULL + b, 256);
+      mbar_init(bar + L::B_REMPTY + b, 1);
+      mbar_init(bar + L::B_DFULL + b, 1);
+      mbar_init(bar + L::B_DEMPTY + b, 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
+  {
+    const int4* g = reinterpret_cast<const int4*>(a.blob);
+    for (int i = threadIdx.x; i < L::BLOB_W1 / 16; i += NTHREADS)
+      reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
+    for (int i = threadIdx.x; i < (L::BLOB_TAIL - L::BLOB_W1) / 16; i += NTHREADS)
+      reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[L::BLOB_W1 / 16 + i];
+    for (int i = threadIdx.x; i < L::TAIL / 16; i += NTHREADS)
+      reinterpret_cast<int4*>(smem + L::OFF_W3)[i] = g[L::BLOB_TAIL / 16 + i];
+    for (int i = threadIdx.x; i < BM * KX; i += NTHREADS) {
+      const int row = i / KX, k = i % KX;
+      *reinterpret_cast<__nv_bfloat16*>(smem + L::OFF_ONES + sw32_offset(row, k)) =
+          __float2bfloat16_rn(k < 2 ? 1.0f : 0.0f);
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const int n_my = (a.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  if (warp >= WARP_LOAD && warp < WARP_MMA) {
+    // ============================================================ loader
+    const int t = threadIdx.x - WARP_LOAD * 32;
+    const uint32_t xbase = smem_u32(smem + L::OFF_X);
+    if (a.x_fast != nullptr) {
+      float4 cur[4], nxt[4];
+      auto load_tile = [&](int it, float4(&v)[4]) {
+        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+        const int64_t row0 = a.r0 + tile * BM;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int idx = t + 128 * i;
+          const int64_t row = row0 + (idx >> 2);
+          v[i] = row < a.r1 ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      if (n_my > 0) load_tile(0, cur);
+      for (int it = 0; it < n_my; ++it) {
+        if (it + 1 < n_my) load_tile(it + 1, nxt);
+        const int s = it % L::XS;
+        mbar_wait(bar + L::B_XEMPTY + s, ((it / L::XS) & 1) ^ 1);
+        const uint32_t xs = xbase + s * L::X_STAGE;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int idx = t + 128 * i;
+          st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(cur[i].x, cur[i].y),
+                       pack_bf16(cur[i].z, cur[i].w));
+        }
+        fence_async_smem();
+        mbar_arrive(bar + L::B_XFULL + s);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+      }
+    } else {
+      float cur[16], nxt[16];
+      auto load_row = [&](int it, float(&v)[16]) {
+        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+        const int64_t row = a.r0 + tile * BM + t;
+#pragma unroll
+        for (int f = 0; f < 16; ++f) v[f] = 0.0f;
+        if (row >= a.r1) return;
+        if (Pin.uniform) {
+          const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
+          const void* base = src.p[Pin.uarray];
+          const int dt = src.dt[Pin.uarray];
+#pragma unroll
+          for (int f = 0; f < 16; ++f)
+            if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
+        } else {
+          uint32_t idx[SMLRT_MAX_SWEEP];
+          unravel(Pin, (uint32_t)row, idx);
+#pragma unroll
+          for (int f = 0; f < 16; ++f)
+            if (f < a.F) {
+              const int arr = __ldg(Pin.col_arr + f);
+              v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
+            }
+        }
+      };
+      if (n_my > 0) load_row(0, cur);
+      for (int it = 0; it < n_my; ++it) {
+        if (it + 1 < n_my) load_row(it + 1, nxt);
+        const int s = it % L::XS;
+        mbar_wait(bar + L::B_XEMPTY + s, ((it / L::XS) & 1) ^ 1);
+        const uint32_t xs = xbase + s * L::X_STAGE;
+        st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
+                     pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
+        st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
+                     pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
+        fence_async_smem();
+        mbar_arrive(bar + L::B_XFULL + s);
+#pragma unroll
+        for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    // ========================================================= MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc1 = idesc_bf16(BM, CH);
+      constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
+      const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
+      const uint64_t w1d0 = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
+      const uint64_t w1bd0 = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
+      const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
+      const uint64_t w2d0 = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
+      const uint64_t xd0 = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
+      auto issue_l2 = [&](int h) {
+        const int j = h / L::NCH, c = h % L::NCH, slot = h & 1;
+        mbar_wait(bar + L::B_RFULL + slot, (h >> 1) & 1);
+        if (c == 0) mbar_wait(bar + L::B_DEMPTY + (j & 1), ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + L::T_D + (j & 1) * H2;
+        if (c == 0) mma_bf16(d, onesd, w2bd, idesc2, 0);  // D = b2
+        const uint32_t ra = tbase + L::T_R + slot * (CH / 2);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ts(d, ra + k * 8, w2d0 + ((c * L::W2_CHUNK + k * 32) >> 4), idesc2, 1);
+        mma_commit(bar + L::B_REMPTY + slot);
+        if (c == L::NCH - 1) mma_commit(bar + L::B_DFULL + (j & 1));
+      };
+      int g = 0;
+      for (int it = 0; it < n_my; ++it) {
+        const int s = it % L::XS;
+        mbar_wait(bar + L::B_XFULL + s, (it / L::XS) & 1);
+        const uint64_t xd = xd0 + ((s * L::X_STAGE) >> 4);
+        for (int c = 0; c < L::NCH; ++c, ++g) {
+          const int slot = g & 1;
+          mbar_wait(bar + L::B_SEMPTY + slot, ((g >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tbase + L::T_S + slot * CH;
+          mma_bf16(d, onesd, w1bd0 + ((c * L::W1_CHUNK) >> 4), idesc1, 0);  // D = b1 (chunk)
+          mma_bf16(d, xd, w1d0 + ((c * L::W1_CHUNK) >> 4), idesc1, 1);
+          mma_commit(bar + L::B_SFULL + slot);
+          if (c == L::NCH - 1) mma_commit(bar + L::B_XEMPTY + s);
+          if (g > 0) issue_l2(g - 1);
+        }
+      }
+      if (g > 0) issue_l2(g - 1);
+    }
+    __syncwarp();
+  } else if (warp >= WARP_EPI1) {
+    // ======================================================== epilogue 1
+    // warpgroup wg handles columns [32 wg, 32 wg + 32) of each 64-wide chunk
+    const int wg = (warp - WARP_EPI1) >> 2, q = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int total = n_my * L::NCH;
+    for (int g = 0; g < total; ++g) {
+      const int slot = g & 1, ph = (g >> 1) & 1;
+      mbar_wait(bar + L::B_SFULL + slot, ph);
+      mbar_wait(bar + L::B_REMPTY + slot, ph ^ 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(tbase + lane_off + L::T_S + slot * CH + wg * 32, v);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar + L::B_SEMPTY + slot);
+      uint32_t p[16];
+      const float* f = reinterpret_cast<const float*>(v);
+      if (a.act1 == SMLRT_RELU) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[e] = pack_relu_bf16(f[2 * e], f[2 * e + 1]);
+      } else if (a.act1 == SMLRT_TANH) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[e] = pack_bf16(tanhf(f[2 * e]), tanhf(f[2 * e + 1]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[e] = pack_bf16(f[2 * e], f[2 * e + 1]);
+      }
+      tmem_st16(tbase + lane_off + L::T_R + slot * (CH / 2) + wg * 16, p);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar + L::B_RFULL + slot);
+    }
+  } else {
+    // ======================================================== epilogue 2
+    const int q = warp, r = q * 32 + lane;
+    const uint32_t w3 = smem_u32(smem + L::OFF_W3);
+    const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
+    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_D;
+    const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 &&
+                          a.staged == nullptr;
+    float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
+                               : nullptr;
+    for (int it = 0; it < n_my; ++it) {
+      const int b = it & 1;
+      mbar_wait(bar + L::B_DFULL + b, (it >> 1) & 1);
+      tc_fence_after();
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int cc = 0; cc < H2 / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(lane_addr + b * H2 + cc * 32, v);
+        tmem_wait_ld();
+        if (cc == H2 / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(bar + L::B_DEMPTY + b);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 ww = ld_shared_f4(w3 + (cc * 32 + e) * 4);
+          const int o = ((e >> 2) & 1) * 4;
+          if (a.act2 == SMLRT_RELU) {
+            acc[o] = fmaf(relu_nan(__uint_as_float(v[e])), ww.x, acc[o]);
+            acc[o + 1] = fmaf(relu_nan(__uint_as_float(v[e + 1])), ww.y, acc[o + 1]);
+            acc[o + 2] = fmaf(relu_nan(__uint_as_float(v[e + 2])), ww.z, acc[o + 2]);
+            acc[o + 3] = fmaf(relu_nan(__uint_as_float(v[e + 3])), ww.w, acc[o + 3]);
+          } else {
+            acc[o] = fmaf(act_f(__uint_as_float(v[e]), a.act2), ww.x, acc[o]);
+            acc[o + 1] = fmaf(act_f(__uint_as_float(v[e + 1]), a.act2), ww.y, acc[o + 1]);
+            acc[o + 2] = fmaf(act_f(__uint_as_float(v[e + 2]), a.act2), ww.z, acc[o + 2]);
+            acc[o + 3] = fmaf(act_f(__uint_as_float(v[e + 3]), a.act2), ww.w, acc[o + 3]);
+          }
+        }
+      }
+      const float y =
+          act_f(((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + b3, a.act3);
+      const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+      const int64_t row = a.r0 + tile * BM + r;
+      bool bad = false;
+      if (row < a.r1) {
+        bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
+        if (out_fast) {
+          out_base[row * Pout.ustride[0]] = y;
+        } else if (a.staged != nullptr) {
+          a.staged[row - a.r0] = y;
+        } else {
+          int64_t addr;
+          int arr;
+          if (Pout.uniform) {
+            addr = Pout.col_off0 + row_offset_uniform(Pout, (uint32_t)row);
+            arr = Pout.uarray;
+          } else {
+            uint32_t idx[SMLRT_MAX_SWEEP];
+            unravel(Pout, (uint32_t)row, idx);
+            addr = col_address(Pout, 0, idx);
+            arr = __ldg(Pout.col_arr);
+          }
+          void* base = const_cast<void*>(dst.p[arr]);
+          if (dst.dt[arr] == SMLRT_F32)
+            reinterpret_cast<float*>(base)[addr] = y;
+          else
+            reinterpret_cast<double*>(base)[addr] = (double)y;
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+// TS self-test: D[128 x N] = A[128 x K] * B[N x K]^T with A staged in TMEM by
+// tcgen05.st (bf16 pairs) exactly as the v2 epilogue stages activations.
+template <int N>
+__global__ void __launch_bounds__(128, 1) tc_selftest_ts_kernel(const float* A, const float* B, int K, float* D) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sb = smem;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sb + N * K * 2);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < N * K; i += 128) {
+    const int r = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sb + (k / 64) * (N * 128) + sw128_offset(r, k & 63)) = __float2bfloat16_rn(B[i]);
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc(slot, 512);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *slot;
+  const int r = warp * 32 + lane;
+  const uint32_t a_col = 256;  // A at columns [256, 256 + K/2), D at [0, N)
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    uint32_t p[16];
+    for (int e = 0; e < 16; ++e) p[e] = pack_bf16(A[r * K + k0 + 2 * e], A[r * K + k0 + 2 * e + 1]);
+    tmem_st16(tbase + ((uint32_t)(warp * 32) << 16) + a_col + k0 / 2, p);
+  }
+  tmem_wait_st();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint64_t bd = smem_desc(smem_u32(sb), 1024, kSwizzle128);
+    for (int kc = 0; kc < K / 64; ++kc)
+      for (int k = 0; k < 4; ++k)
+        mma_bf16_ts(tbase, tbase + a_col + kc * 32 + k * 8, bd + ((kc * N * 128 + k * 32) >> 4),
+                    idesc_bf16(128, N), (kc | k) != 0);
+    mma_commit(bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + c0, v);
+    tmem_wait_ld();
+    for (int e = 0; e < 32; ++e) D[r * N + c0 + e] = __uint_as_float(v[e]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 // ---------------------------------------------------------- host helpers --
 uint16_t f2bf(float f) {
   uint32_t u;
@@ -498,17 +896,33 @@ int num_sms() {
   return n;
 }
 
+bool use_v2() {
+  static int v = -1;
+  if (v < 0) {
+    // v1 (SMEM A2, per-tile handshakes) is the default; v2 (TMEM A2, 64-wide
+    // chunk streaming) is correct but latency-bound at one MMA->epilogue->MMA
+    // round trip per 320 tensor cycles.  SMLRT_TC_VARIANT=v2 selects it.
+    const char* e = getenv("SMLRT_TC_VARIANT");
+    v = (e != nullptr && e[0] == 'v' && e[1] == '2') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int H1, int H2>
 int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
            int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
            int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   using L = Lay<H1, H2>;
+  const bool v2 = use_v2() && H2 <= 128;
   if (n_in > 8 || n_out > 8) return SMLRT_E_UNSUPPORTED;
   static int configured_mask = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured_mask & (1 << dev))) {
     SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC));
+    if constexpr (H2 <= 128)
+      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      LayTS<H1, H2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
@@ -538,6 +952,13 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
   const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
+  if constexpr (H2 <= 128) {
+    if (v2) {
+      mlp3_ts_kernel<H1, H2><<<grid, NTHREADS, LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
+      SMLRT_CUDA(cudaGetLastError());
+      return SMLRT_OK;
+    }
+  }
   mlp3_tc_kernel<H1, H2><<<grid, NTHREADS, L::ALLOC, s>>>(a, in, src, out, dst);
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
@@ -657,6 +1078,36 @@ extern "C" int smlrt_tc_selftest(int K, int N, const float* A, const float* B, f
   } else {
     SMLRT_CUDA(cudaFuncSetAttribute(tc_selftest_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     tc_selftest_kernel<256><<<1, 128, smem>>>(dA, dB, K, dD);
+  }
+  SMLRT_CUDA(cudaGetLastError());
+  SMLRT_CUDA(cudaDeviceSynchronize());
+  SMLRT_CUDA(cudaMemcpy(D, dD, 128 * N * 4, cudaMemcpyDeviceToHost));
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dD);
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_tc_selftest_ts(int K, int N, const float* A, const float* B, float* D) {
+  using namespace smlrt;
+  if (!(K % 64 == 0 && K <= 256) || !(N == 64 || N == 128 || N == 256))
+    return fail(SMLRT_E_INVALID, "tc_selftest_ts: K in {64,128,192,256}, N in {64,128,256}");
+  float *dA, *dB, *dD;
+  SMLRT_CUDA(cudaMalloc(&dA, 128 * K * 4));
+  SMLRT_CUDA(cudaMalloc(&dB, N * K * 4));
+  SMLRT_CUDA(cudaMalloc(&dD, 128 * N * 4));
+  SMLRT_CUDA(cudaMemcpy(dA, A, 128 * K * 4, cudaMemcpyHostToDevice));
+  SMLRT_CUDA(cudaMemcpy(dB, B, N * K * 4, cudaMemcpyHostToDevice));
+  const int smem = N * K * 2 + 64 + 1024;
+  if (N == 64) {
+    SMLRT_CUDA(cudaFuncSetAttribute(tc_selftest_ts_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    tc_selftest_ts_kernel<64><<<1, 128, smem>>>(dA, dB, K, dD);
+  } else if (N == 128) {
+    SMLRT_CUDA(cudaFuncSetAttribute(tc_selftest_ts_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    tc_selftest_ts_kernel<128><<<1, 128, smem>>>(dA, dB, K, dD);
+  } else {
+    SMLRT_CUDA(cudaFuncSetAttribute(tc_selftest_ts_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    tc_selftest_ts_kernel<256><<<1, 128, smem>>>(dA, dB, K, dD);
   }
   SMLRT_CUDA(cudaGetLastError());
   SMLRT_CUDA(cudaDeviceSynchronize());

@@ -29,6 +29,16 @@ def test_selftest_gemm(cuda, K, N):
     assert np.max(np.abs(D - want)) <= 1e-4 * max(1.0, np.abs(want).max()), np.abs(D - want).max()
 
 
+@pytest.mark.parametrize("K,N", [(64, 128), (256, 128), (128, 64), (64, 256)])
+def test_selftest_gemm_tmem_a(cuda, K, N):
+    rng = np.random.default_rng(K * 7 + N)
+    A = rng.normal(size=(128, K)).astype(np.float32)
+    B = rng.normal(size=(N, K)).astype(np.float32)
+    D = _native.tc_selftest(A, B, tmem_a=True)
+    want = bf16(A) @ bf16(B).T
+    assert np.max(np.abs(D - want)) <= 1e-4 * max(1.0, np.abs(want).max()), np.abs(D - want).max()
+
+
 def emulate_bf16(layers, x):
     """bf16 operands, f32-ish accumulation, bf16 hidden re-quantisation of
     layer-1 output, f32 epilogue for the last two layers (as the kernel)."""
