@@ -152,8 +152,9 @@ def _inner_rows(wl):
     return int(np.prod([s.count for s in ti.slices[1:]])) if len(ti.slices) > 1 else 1
 
 
-# CPU sample per config: about 10-20 s of reference-path work on one core
-CPU_SAMPLE = {"options": 1_000_000, "bonds": 65_536, "minibude": 2_048, "miniweather": 4094 * 2046}
+# CPU sample per config (first sweep rows): a few seconds of reference-path
+# work over all host cores; full size for C1 and C5
+CPU_SAMPLE = {"options": 1_000_000, "bonds": 262_144, "minibude": 16_384, "miniweather": 4094 * 2046}
 
 
 def _cpu_sample_elems(name):
