@@ -438,29 +438,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ============================================================================
-// v2: layer-2 A operand from TMEM ("TS" MMA), layer 1 streamed in 64-feature
-// chunks.  Per chunk g (tile i = g / NCH, chunk c = g % NCH):
-//   MMA   L1c : S[g&1] = ones*W1B_c + X_i*W1_c          (M=128, N=64, SMEM operands)
-//   epi1      : S[g&1] -> act -> bf16 pairs -> tcgen05.st -> R[g&1]   (no SMEM)
-//   MMA   L2c : D[i&1] (+)= R[g&1] * W2_c  (4 x K=16, A from TMEM); c==0 adds ones*W2B
-//   epi2      : D[i&1] -> act -> dot w3 -> +b3 -> scatter
-// TMEM: S 2x64 + R 2x32 + D 2xH2 <= 512 columns.  SMEM holds only weights,
-// the ones tile and the X ring, and the tensor core reads only the B operand
-// (weights) from it for layer 2 -- the operand stream that saturated the
-// SMEM port in v1 (A2 reads + the epilogue's A2 writes) is gone.
-constexpr int CH = 64;
-
+// v3: two tiles in flight in two 256-column TMEM regions; layer-2 A operand
+// from TMEM.  Per tile i (region P = i & 1, base column RB = 256 P):
+//   MMA  L1 : P[0,H1) = ones*W1B + X_i*W1                       (N = H1, SMEM operands)
+//   epi1    : warpgroup w converts fp32 columns [w H1/2, (w+1) H1/2) to act+bf16 pairs
+//             IN PLACE: slab s (32 cols) -> 16 packed cols at w H1/2 + 16 s (always
+//             columns this thread already drained); signals A2S[P][s] per slab
+//   MMA  L2 : two N = H2/2 halves, D2a at P[H1/4, ..), D2b at P[3 H1/4, ..) (drained
+//             columns), A = packed activations in TMEM (TS form), K-steps issued as
+//             soon as their slab is ready; bias via ones*W2B
+//   epi2    : D2a|D2b -> act -> dot w3 -> +b3 -> scatter; frees region P
+// MMAs are issued tile-pairwise (L1 L1 L2 L2) so each epilogue overlaps the
+// other tile's tensor work.  SMEM carries only weights, the ones tile and the
+// X ring: the tensor core reads A2 from TMEM and the epilogue never stores to
+// SMEM.  Requires H1 == 256 (region width) and H2 <= H1 / 2.
 template <int H1, int H2>
-struct LayTS {
-  static_assert(H1 % CH == 0 && H1 >= CH && H1 <= 256, "H1: multiple of 64, <= 256");
-  static_assert(H2 % 32 == 0 && H2 >= 32 && 4 * CH + 2 * H2 <= 512, "H2 <= 128 (TMEM)");
-  static constexpr int NCH = H1 / CH;
-  static constexpr int W2_CHUNK = H2 * 128;  // [H2][64] bf16 SW128 (K chunk c of W2)
-  static constexpr int W1_CHUNK = CH * 32;   // [64][16] bf16 SW32 (rows 64c.. of W1)
+struct LayV3 {
+  static_assert(H1 == 256, "v3: H1 must equal the 256-column TMEM region");
+  static_assert(H2 % 32 == 0 && H2 >= 32 && H2 <= H1 / 2, "v3: H2 <= H1/2");
+  static constexpr int KC = H1 / 64;          // W2 K chunks of 64 (SW128)
+  static constexpr int W2_CHUNK = H2 * 128;
   static constexpr int X_STAGE = BM * 32;
   static constexpr int XS = 4;
   static constexpr int OFF_W2 = 0;
-  static constexpr int OFF_W1 = OFF_W2 + NCH * W2_CHUNK;
+  static constexpr int OFF_W1 = OFF_W2 + KC * W2_CHUNK;
   static constexpr int OFF_W1B = OFF_W1 + H1 * 32;
   static constexpr int OFF_W2B = OFF_W1B + H1 * 32;
   static constexpr int OFF_ONES = OFF_W2B + H2 * 32;
@@ -468,33 +469,31 @@ struct LayTS {
   static constexpr int OFF_W3 = OFF_X + XS * X_STAGE;
   static constexpr int OFF_B3 = OFF_W3 + H2 * 4;
   static constexpr int OFF_BAR = OFF_B3 + 16;
+  static constexpr int NSLAB = H1 / 2 / 32;   // slabs per warpgroup
   enum {
     B_XFULL = 0,
     B_XEMPTY = XS,
-    B_SFULL = 2 * XS,
-    B_SEMPTY = B_SFULL + 2,
-    B_RFULL = B_SEMPTY + 2,
-    B_REMPTY = B_RFULL + 2,
-    B_DFULL = B_REMPTY + 2,
-    B_DEMPTY = B_DFULL + 2,
-    N_BAR = B_DEMPTY + 2
+    B_L1FULL = 2 * XS,
+    B_A2S = B_L1FULL + 2,             // [2][NSLAB]
+    B_D2FULL = B_A2S + 2 * NSLAB,
+    B_FREE = B_D2FULL + 2,
+    N_BAR = B_FREE + 2
   };
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
   static_assert(ALLOC <= 232448, "shared memory budget");
-  // blob (same layout as v1's pack): W2 | W1 | W1B | W2B | w3 | b3
-  static constexpr int BLOB_W1 = NCH * W2_CHUNK;
+  static constexpr int BLOB_W1 = KC * W2_CHUNK;
   static constexpr int BLOB_TAIL = BLOB_W1 + 2 * H1 * 32 + H2 * 32;
   static constexpr int TAIL = H2 * 4 + 16;
-  static constexpr int T_S = 0, T_R = 2 * CH, T_D = 3 * CH + CH;  // D at column 256
+  static constexpr int D2A = H1 / 4, D2B = 3 * H1 / 4;  // column offsets inside a region
 };
 
 template <int H1, int H2>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    mlp3_ts_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
+    mlp3_v3_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
                    const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
                    const __grid_constant__ Ptrs8 dst) {
-  using L = LayTS<H1, H2>;
+  using L = LayV3<H1, H2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -507,12 +506,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(bar + L::B_XEMPTY + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar + L::B_SFULL + b, 1);
-      mbar_init(bar + L::B_SEMPTY + b, 256);
-      mbar_init(bar + L::B_RFULL + b, 256);
-      mbar_init(bar + L::B_REMPTY + b, 1);
-      mbar_init(bar + L::B_DFULL + b, 1);
-      mbar_init(bar + L::B_DEMPTY + b, 128);
+      mbar_init(bar + L::B_L1FULL + b, 1);
+      for (int s = 0; s < L::NSLAB; ++s) mbar_init(bar + L::B_A2S + b * L::NSLAB + s, 256);
+      mbar_init(bar + L::B_D2FULL + b, 1);
+      mbar_init(bar + L::B_FREE + b, 128);
     }
     mbar_fence_init();
   }
@@ -535,7 +532,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int n_my = (a.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
   if (warp >= WARP_LOAD && warp < WARP_MMA) {
@@ -615,106 +612,111 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == WARP_MMA) {
-    // ========================================================= MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc1 = idesc_bf16(BM, CH);
-      constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
-      const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
-      const uint64_t w1d0 = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
-      const uint64_t w1bd0 = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
-      const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
-      const uint64_t w2d0 = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
-      const uint64_t xd0 = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
-      auto issue_l2 = [&](int h) {
-        const int j = h / L::NCH, c = h % L::NCH, slot = h & 1;
-        mbar_wait(bar + L::B_RFULL + slot, (h >> 1) & 1);
-        if (c == 0) mbar_wait(bar + L::B_DEMPTY + (j & 1), ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tbase + L::T_D + (j & 1) * H2;
-        if (c == 0) mma_bf16(d, onesd, w2bd, idesc2, 0);  // D = b2
-        const uint32_t ra = tbase + L::T_R + slot * (CH / 2);
+    // ================================================ MMA issuer (whole warp)
+    constexpr uint32_t idesc1 = idesc_bf16(BM, H1);
+    constexpr uint32_t idesc2 = idesc_bf16(BM, H2 / 2);
+    const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
+    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
+    const uint64_t w1bd = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
+    const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
+    const uint64_t w2d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
+    const uint64_t xd0 = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
+    auto issue_l1 = [&](int t) {
+      const int reg = t & 1, s = t % L::XS;
+      mbar_wait(bar + L::B_XFULL + s, (t / L::XS) & 1);
+      mbar_wait(bar + L::B_FREE + reg, ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tbase + reg * 256;
+      mma_ss_elect(d, onesd, w1bd, idesc1, 0);
+      mma_ss_elect(d, xd0 + ((s * L::X_STAGE) >> 4), w1d, idesc1, 1);
+      mma_commit_elect(bar + L::B_XEMPTY + s);
+      mma_commit_elect(bar + L::B_L1FULL + reg);
+    };
+    auto issue_l2 = [&](int t) {
+      const int reg = t & 1, ph = (t >> 1) & 1;
+      const uint32_t rb = tbase + reg * 256;
+      const uint32_t da = rb + L::D2A, db = rb + L::D2B;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_bf16_ts(d, ra + k * 8, w2d0 + ((c * L::W2_CHUNK + k * 32) >> 4), idesc2, 1);
-        mma_commit(bar + L::B_REMPTY + slot);
-        if (c == L::NCH - 1) mma_commit(bar + L::B_DFULL + (j & 1));
-      };
-      int g = 0;
-      for (int it = 0; it < n_my; ++it) {
-        const int s = it % L::XS;
-        mbar_wait(bar + L::B_XFULL + s, (it / L::XS) & 1);
-        const uint64_t xd = xd0 + ((s * L::X_STAGE) >> 4);
-        for (int c = 0; c < L::NCH; ++c, ++g) {
-          const int slot = g & 1;
-          mbar_wait(bar + L::B_SEMPTY + slot, ((g >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t d = tbase + L::T_S + slot * CH;
-          mma_bf16(d, onesd, w1bd0 + ((c * L::W1_CHUNK) >> 4), idesc1, 0);  // D = b1 (chunk)
-          mma_bf16(d, xd, w1d0 + ((c * L::W1_CHUNK) >> 4), idesc1, 1);
-          mma_commit(bar + L::B_SFULL + slot);
-          if (c == L::NCH - 1) mma_commit(bar + L::B_XEMPTY + s);
-          if (g > 0) issue_l2(g - 1);
+      for (int sl = 0; sl < L::NSLAB; ++sl) {
+        mbar_wait(bar + L::B_A2S + reg * L::NSLAB + sl, ph);
+        tc_fence_after();
+        if (sl == 0) {
+          mma_ss_elect(da, onesd, w2bd, idesc2, 0);
+          mma_ss_elect(db, onesd, w2bd + ((H2 / 2 * 32) >> 4), idesc2, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          // K-steps 2 sl, 2 sl + 1 (warpgroup 0) and 8 + 2 sl, 9 + 2 sl (warpgroup 1)
+          const int k = (j < 2) ? (2 * sl + j) : (H1 / 32 + 2 * sl + (j - 2));
+          const uint32_t at = rb + ((k < H1 / 32) ? 8 * k : H1 / 2 + 8 * (k - H1 / 32));
+          const uint32_t boff = (k >> 2) * L::W2_CHUNK + (k & 3) * 32;
+          mma_ts_elect(da, at, w2d + (boff >> 4), idesc2, 1);
+          mma_ts_elect(db, at, w2d + ((boff + H2 / 2 * 128) >> 4), idesc2, 1);
         }
       }
-      if (g > 0) issue_l2(g - 1);
+      mma_commit_elect(bar + L::B_D2FULL + reg);
+    };
+    for (int t = 0; t < n_my; t += 2) {
+      issue_l1(t);
+      if (t + 1 < n_my) issue_l1(t + 1);
+      issue_l2(t);
+      if (t + 1 < n_my) issue_l2(t + 1);
     }
-    __syncwarp();
   } else if (warp >= WARP_EPI1) {
     // ======================================================== epilogue 1
-    // warpgroup wg handles columns [32 wg, 32 wg + 32) of each 64-wide chunk
     const int wg = (warp - WARP_EPI1) >> 2, q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int total = n_my * L::NCH;
-    for (int g = 0; g < total; ++g) {
-      const int slot = g & 1, ph = (g >> 1) & 1;
-      mbar_wait(bar + L::B_SFULL + slot, ph);
-      mbar_wait(bar + L::B_REMPTY + slot, ph ^ 1);
+    for (int t = 0; t < n_my; ++t) {
+      const int reg = t & 1;
+      mbar_wait(bar + L::B_L1FULL + reg, (t >> 1) & 1);
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tbase + lane_off + L::T_S + slot * CH + wg * 32, v);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar + L::B_SEMPTY + slot);
-      uint32_t p[16];
-      const float* f = reinterpret_cast<const float*>(v);
-      if (a.act1 == SMLRT_RELU) {
+      const uint32_t cb = tbase + lane_off + reg * 256 + wg * (H1 / 2);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) p[e] = pack_relu_bf16(f[2 * e], f[2 * e + 1]);
-      } else if (a.act1 == SMLRT_TANH) {
+      for (int sl = 0; sl < L::NSLAB; ++sl) {
+        uint32_t v[32], p[16];
+        tmem_ld32(cb + sl * 32, v);
+        tmem_wait_ld();
+        const float* f = reinterpret_cast<const float*>(v);
+        if (a.act1 == SMLRT_RELU) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) p[e] = pack_bf16(tanhf(f[2 * e]), tanhf(f[2 * e + 1]));
-      } else {
+          for (int e = 0; e < 16; ++e) p[e] = pack_relu_bf16(f[2 * e], f[2 * e + 1]);
+        } else if (a.act1 == SMLRT_TANH) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) p[e] = pack_bf16(f[2 * e], f[2 * e + 1]);
+          for (int e = 0; e < 16; ++e) p[e] = pack_bf16(tanhf(f[2 * e]), tanhf(f[2 * e + 1]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) p[e] = pack_bf16(f[2 * e], f[2 * e + 1]);
+        }
+        tmem_st16(cb + sl * 16, p);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar + L::B_A2S + reg * L::NSLAB + sl);
       }
-      tmem_st16(tbase + lane_off + L::T_R + slot * (CH / 2) + wg * 16, p);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar + L::B_RFULL + slot);
     }
   } else {
     // ======================================================== epilogue 2
     const int q = warp, r = q * 32 + lane;
     const uint32_t w3 = smem_u32(smem + L::OFF_W3);
     const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
-    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_D;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 &&
                           a.staged == nullptr;
     float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
                                : nullptr;
-    for (int it = 0; it < n_my; ++it) {
-      const int b = it & 1;
-      mbar_wait(bar + L::B_DFULL + b, (it >> 1) & 1);
+    for (int t = 0; t < n_my; ++t) {
+      const int reg = t & 1;
+      mbar_wait(bar + L::B_D2FULL + reg, (t >> 1) & 1);
       tc_fence_after();
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int cc = 0; cc < H2 / 32; ++cc) {
         uint32_t v[32];
-        tmem_ld32(lane_addr + b * H2 + cc * 32, v);
+        const int half = cc / (H2 / 64), within = cc % (H2 / 64);
+        tmem_ld32(tbase + lane_off + reg * 256 + (half ? L::D2B : L::D2A) + within * 32, v);
         tmem_wait_ld();
         if (cc == H2 / 32 - 1) {
           tc_fence_before();
-          mbar_arrive(bar + L::B_DEMPTY + b);
+          mbar_arrive(bar + L::B_FREE + reg);
         }
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
@@ -735,7 +737,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       const float y =
           act_f(((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + b3, a.act3);
-      const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+      const int64_t tile = (int64_t)blockIdx.x + (int64_t)t * gridDim.x;
       const int64_t row = a.r0 + tile * BM + r;
       bool bad = false;
       if (row < a.r1) {
@@ -899,11 +901,10 @@ int num_sms() {
 bool use_v2() {
   static int v = -1;
   if (v < 0) {
-    // v1 (SMEM A2, per-tile handshakes) is the default; v2 (TMEM A2, 64-wide
-    // chunk streaming) is correct but latency-bound at one MMA->epilogue->MMA
-    // round trip per 320 tensor cycles.  SMLRT_TC_VARIANT=v2 selects it.
+    // v3 (TMEM A operand, two tiles in flight) is the default where the
+    // shape allows it; SMLRT_TC_VARIANT=v1 forces the SMEM-A2 kernel.
     const char* e = getenv("SMLRT_TC_VARIANT");
-    v = (e != nullptr && e[0] == 'v' && e[1] == '2') ? 1 : 0;
+    v = (e != nullptr && e[0] == 'v' && e[1] == '1') ? 0 : 1;
   }
   return v == 1;
 }
@@ -913,16 +914,17 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
            int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
            int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   using L = Lay<H1, H2>;
-  const bool v2 = use_v2() && H2 <= 128;
+  constexpr bool v3_ok = (H1 == 256 && H2 <= H1 / 2);
+  const bool v3 = use_v2() && v3_ok;
   if (n_in > 8 || n_out > 8) return SMLRT_E_UNSUPPORTED;
   static int configured_mask = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured_mask & (1 << dev))) {
     SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC));
-    if constexpr (H2 <= 128)
-      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      LayTS<H1, H2>::ALLOC));
+    if constexpr (v3_ok)
+      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_v3_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      LayV3<H1, H2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
@@ -952,9 +954,9 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
   const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-  if constexpr (H2 <= 128) {
-    if (v2) {
-      mlp3_ts_kernel<H1, H2><<<grid, NTHREADS, LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
+  if constexpr (v3_ok) {
+    if (v3) {
+      mlp3_v3_kernel<H1, H2><<<grid, NTHREADS, LayV3<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
       SMLRT_CUDA(cudaGetLastError());
       return SMLRT_OK;
     }
