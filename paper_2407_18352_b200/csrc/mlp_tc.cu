@@ -437,348 +437,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-// ============================================================================
-// v3: two tiles in flight in two 256-column TMEM regions; layer-2 A operand
-// from TMEM.  Per tile i (region P = i & 1, base column RB = 256 P):
-//   MMA  L1 : P[0,H1) = ones*W1B + X_i*W1                       (N = H1, SMEM operands)
-//   epi1    : warpgroup w converts fp32 columns [w H1/2, (w+1) H1/2) to act+bf16 pairs
-//             IN PLACE: slab s (32 cols) -> 16 packed cols at w H1/2 + 16 s (always
-//             columns this thread already drained); signals A2S[P][s] per slab
-//   MMA  L2 : two N = H2/2 halves, D2a at P[H1/4, ..), D2b at P[3 H1/4, ..) (drained
-//             columns), A = packed activations in TMEM (TS form), K-steps issued as
-//             soon as their slab is ready; bias via ones*W2B
-//   epi2    : D2a|D2b -> act -> dot w3 -> +b3 -> scatter; frees region P
-// MMAs are issued tile-pairwise (L1 L1 L2 L2) so each epilogue overlaps the
-// other tile's tensor work.  SMEM carries only weights, the ones tile and the
-// X ring: the tensor core reads A2 from TMEM and the epilogue never stores to
-// SMEM.  Requires H1 == 256 (region width) and H2 <= H1 / 2.
-template <int H1, int H2>
-struct LayV3 {
-  static_assert(H1 == 256, "v3: H1 must equal the 256-column TMEM region");
-  static_assert(H2 % 32 == 0 && H2 >= 32 && H2 <= H1 / 2, "v3: H2 <= H1/2");
-  static constexpr int KC = H1 / 64;          // W2 K chunks of 64 (SW128)
-  static constexpr int W2_CHUNK = H2 * 128;
-  static constexpr int X_STAGE = BM * 32;
-  static constexpr int XS = 4;
-  static constexpr int OFF_W2 = 0;
-  static constexpr int OFF_W1 = OFF_W2 + KC * W2_CHUNK;
-  static constexpr int OFF_W1B = OFF_W1 + H1 * 32;
-  static constexpr int OFF_W2B = OFF_W1B + H1 * 32;
-  static constexpr int OFF_ONES = OFF_W2B + H2 * 32;
-  static constexpr int OFF_X = OFF_ONES + BM * 32;
-  static constexpr int OFF_W3 = OFF_X + XS * X_STAGE;
-  static constexpr int OFF_B3 = OFF_W3 + H2 * 4;
-  static constexpr int OFF_BAR = OFF_B3 + 16;
-  static constexpr int NSLAB = H1 / 2 / 32;   // slabs per warpgroup
-  enum {
-    B_XFULL = 0,
-    B_XEMPTY = XS,
-    B_L1FULL = 2 * XS,
-    B_A2S = B_L1FULL + 2,             // [2][NSLAB]
-    B_D2FULL = B_A2S + 2 * NSLAB,
-    B_FREE = B_D2FULL + 2,
-    N_BAR = B_FREE + 2
-  };
-  static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
-  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
-  static_assert(ALLOC <= 232448, "shared memory budget");
-  static constexpr int BLOB_W1 = KC * W2_CHUNK;
-  static constexpr int BLOB_TAIL = BLOB_W1 + 2 * H1 * 32 + H2 * 32;
-  static constexpr int TAIL = H2 * 4 + 16;
-  static constexpr int D2A = H1 / 4, D2B = 3 * H1 / 4;  // column offsets inside a region
-};
-
-template <int H1, int H2>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    mlp3_v3_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
-                   const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
-                   const __grid_constant__ Ptrs8 dst) {
-  using L = LayV3<H1, H2>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < L::XS; ++s) {
-      mbar_init(bar + L::B_XFULL + s, 128);
-      mbar_init(bar + L::B_XEMPTY + s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar + L::B_L1FULL + b, 1);
-      for (int s = 0; s < L::NSLAB; ++s) mbar_init(bar + L::B_A2S + b * L::NSLAB + s, 256);
-      mbar_init(bar + L::B_D2FULL + b, 1);
-      mbar_init(bar + L::B_FREE + b, 128);
-    }
-    mbar_fence_init();
-  }
-  if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
-  {
-    const int4* g = reinterpret_cast<const int4*>(a.blob);
-    for (int i = threadIdx.x; i < L::BLOB_W1 / 16; i += NTHREADS)
-      reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
-    for (int i = threadIdx.x; i < (L::BLOB_TAIL - L::BLOB_W1) / 16; i += NTHREADS)
-      reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[L::BLOB_W1 / 16 + i];
-    for (int i = threadIdx.x; i < L::TAIL / 16; i += NTHREADS)
-      reinterpret_cast<int4*>(smem + L::OFF_W3)[i] = g[L::BLOB_TAIL / 16 + i];
-    for (int i = threadIdx.x; i < BM * KX; i += NTHREADS) {
-      const int row = i / KX, k = i % KX;
-      *reinterpret_cast<__nv_bfloat16*>(smem + L::OFF_ONES + sw32_offset(row, k)) =
-          __float2bfloat16_rn(k < 2 ? 1.0f : 0.0f);
-    }
-  }
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  const int n_my = (a.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-
-  if (warp >= WARP_LOAD && warp < WARP_MMA) {
-    // ============================================================ loader
-    const int t = threadIdx.x - WARP_LOAD * 32;
-    const uint32_t xbase = smem_u32(smem + L::OFF_X);
-    if (a.x_fast != nullptr) {
-      float4 cur[4], nxt[4];
-      auto load_tile = [&](int it, float4(&v)[4]) {
-        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-        const int64_t row0 = a.r0 + tile * BM;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = t + 128 * i;
-          const int64_t row = row0 + (idx >> 2);
-          v[i] = row < a.r1 ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      };
-      if (n_my > 0) load_tile(0, cur);
-      for (int it = 0; it < n_my; ++it) {
-        if (it + 1 < n_my) load_tile(it + 1, nxt);
-        const int s = it % L::XS;
-        mbar_wait(bar + L::B_XEMPTY + s, ((it / L::XS) & 1) ^ 1);
-        const uint32_t xs = xbase + s * L::X_STAGE;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = t + 128 * i;
-          st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(cur[i].x, cur[i].y),
-                       pack_bf16(cur[i].z, cur[i].w));
-        }
-        fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
-      }
-    } else {
-      float cur[16], nxt[16];
-      auto load_row = [&](int it, float(&v)[16]) {
-        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-        const int64_t row = a.r0 + tile * BM + t;
-#pragma unroll
-        for (int f = 0; f < 16; ++f) v[f] = 0.0f;
-        if (row >= a.r1) return;
-        if (Pin.uniform) {
-          const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
-          const void* base = src.p[Pin.uarray];
-          const int dt = src.dt[Pin.uarray];
-#pragma unroll
-          for (int f = 0; f < 16; ++f)
-            if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
-        } else {
-          uint32_t idx[SMLRT_MAX_SWEEP];
-          unravel(Pin, (uint32_t)row, idx);
-#pragma unroll
-          for (int f = 0; f < 16; ++f)
-            if (f < a.F) {
-              const int arr = __ldg(Pin.col_arr + f);
-              v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
-            }
-        }
-      };
-      if (n_my > 0) load_row(0, cur);
-      for (int it = 0; it < n_my; ++it) {
-        if (it + 1 < n_my) load_row(it + 1, nxt);
-        const int s = it % L::XS;
-        mbar_wait(bar + L::B_XEMPTY + s, ((it / L::XS) & 1) ^ 1);
-        const uint32_t xs = xbase + s * L::X_STAGE;
-        st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
-                     pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
-        st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
-                     pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
-        fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
-#pragma unroll
-        for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
-      }
-    }
-  } else if (warp == WARP_MMA) {
-    // ================================================ MMA issuer (whole warp)
-    constexpr uint32_t idesc1 = idesc_bf16(BM, H1);
-    constexpr uint32_t idesc2 = idesc_bf16(BM, H2 / 2);
-    const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
-    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
-    const uint64_t w1bd = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
-    const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
-    const uint64_t w2d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
-    const uint64_t xd0 = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
-    auto issue_l1 = [&](int t) {
-      const int reg = t & 1, s = t % L::XS;
-      mbar_wait(bar + L::B_XFULL + s, (t / L::XS) & 1);
-      mbar_wait(bar + L::B_FREE + reg, ((t >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d = tbase + reg * 256;
-      mma_ss_elect(d, onesd, w1bd, idesc1, 0);
-      mma_ss_elect(d, xd0 + ((s * L::X_STAGE) >> 4), w1d, idesc1, 1);
-      mma_commit_elect(bar + L::B_XEMPTY + s);
-      mma_commit_elect(bar + L::B_L1FULL + reg);
-    };
-    auto issue_l2 = [&](int t) {
-      const int reg = t & 1, ph = (t >> 1) & 1;
-      const uint32_t rb = tbase + reg * 256;
-      const uint32_t da = rb + L::D2A, db = rb + L::D2B;
-#pragma unroll
-      for (int sl = 0; sl < L::NSLAB; ++sl) {
-        mbar_wait(bar + L::B_A2S + reg * L::NSLAB + sl, ph);
-        tc_fence_after();
-        if (sl == 0) {
-          mma_ss_elect(da, onesd, w2bd, idesc2, 0);
-          mma_ss_elect(db, onesd, w2bd + ((H2 / 2 * 32) >> 4), idesc2, 0);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // K-steps 2 sl, 2 sl + 1 (warpgroup 0) and 8 + 2 sl, 9 + 2 sl (warpgroup 1)
-          const int k = (j < 2) ? (2 * sl + j) : (H1 / 32 + 2 * sl + (j - 2));
-          const uint32_t at = rb + ((k < H1 / 32) ? 8 * k : H1 / 2 + 8 * (k - H1 / 32));
-          const uint32_t boff = (k >> 2) * L::W2_CHUNK + (k & 3) * 32;
-          mma_ts_elect(da, at, w2d + (boff >> 4), idesc2, 1);
-          mma_ts_elect(db, at, w2d + ((boff + H2 / 2 * 128) >> 4), idesc2, 1);
-        }
-      }
-      mma_commit_elect(bar + L::B_D2FULL + reg);
-    };
-    for (int t = 0; t < n_my; t += 2) {
-      issue_l1(t);
-      if (t + 1 < n_my) issue_l1(t + 1);
-      issue_l2(t);
-      if (t + 1 < n_my) issue_l2(t + 1);
-    }
-  } else if (warp >= WARP_EPI1) {
-    // ======================================================== epilogue 1
-    const int wg = (warp - WARP_EPI1) >> 2, q = warp & 3;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    for (int t = 0; t < n_my; ++t) {
-      const int reg = t & 1;
-      mbar_wait(bar + L::B_L1FULL + reg, (t >> 1) & 1);
-      tc_fence_after();
-      const uint32_t cb = tbase + lane_off + reg * 256 + wg * (H1 / 2);
-#pragma unroll
-      for (int sl = 0; sl < L::NSLAB; ++sl) {
-        uint32_t v[32], p[16];
-        tmem_ld32(cb + sl * 32, v);
-        tmem_wait_ld();
-        const float* f = reinterpret_cast<const float*>(v);
-        if (a.act1 == SMLRT_RELU) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) p[e] = pack_relu_bf16(f[2 * e], f[2 * e + 1]);
-        } else if (a.act1 == SMLRT_TANH) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) p[e] = pack_bf16(tanhf(f[2 * e]), tanhf(f[2 * e + 1]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) p[e] = pack_bf16(f[2 * e], f[2 * e + 1]);
-        }
-        tmem_st16(cb + sl * 16, p);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(bar + L::B_A2S + reg * L::NSLAB + sl);
-      }
-    }
-  } else {
-    // ======================================================== epilogue 2
-    const int q = warp, r = q * 32 + lane;
-    const uint32_t w3 = smem_u32(smem + L::OFF_W3);
-    const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 &&
-                          a.staged == nullptr;
-    float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
-                               : nullptr;
-    for (int t = 0; t < n_my; ++t) {
-      const int reg = t & 1;
-      mbar_wait(bar + L::B_D2FULL + reg, (t >> 1) & 1);
-      tc_fence_after();
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int cc = 0; cc < H2 / 32; ++cc) {
-        uint32_t v[32];
-        const int half = cc / (H2 / 64), within = cc % (H2 / 64);
-        tmem_ld32(tbase + lane_off + reg * 256 + (half ? L::D2B : L::D2A) + within * 32, v);
-        tmem_wait_ld();
-        if (cc == H2 / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(bar + L::B_FREE + reg);
-        }
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 ww = ld_shared_f4(w3 + (cc * 32 + e) * 4);
-          const int o = ((e >> 2) & 1) * 4;
-          if (a.act2 == SMLRT_RELU) {
-            acc[o] = fmaf(relu_nan(__uint_as_float(v[e])), ww.x, acc[o]);
-            acc[o + 1] = fmaf(relu_nan(__uint_as_float(v[e + 1])), ww.y, acc[o + 1]);
-            acc[o + 2] = fmaf(relu_nan(__uint_as_float(v[e + 2])), ww.z, acc[o + 2]);
-            acc[o + 3] = fmaf(relu_nan(__uint_as_float(v[e + 3])), ww.w, acc[o + 3]);
-          } else {
-            acc[o] = fmaf(act_f(__uint_as_float(v[e]), a.act2), ww.x, acc[o]);
-            acc[o + 1] = fmaf(act_f(__uint_as_float(v[e + 1]), a.act2), ww.y, acc[o + 1]);
-            acc[o + 2] = fmaf(act_f(__uint_as_float(v[e + 2]), a.act2), ww.z, acc[o + 2]);
-            acc[o + 3] = fmaf(act_f(__uint_as_float(v[e + 3]), a.act2), ww.w, acc[o + 3]);
-          }
-        }
-      }
-      const float y =
-          act_f(((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + b3, a.act3);
-      const int64_t tile = (int64_t)blockIdx.x + (int64_t)t * gridDim.x;
-      const int64_t row = a.r0 + tile * BM + r;
-      bool bad = false;
-      if (row < a.r1) {
-        bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
-        if (out_fast) {
-          out_base[row * Pout.ustride[0]] = y;
-        } else if (a.staged != nullptr) {
-          a.staged[row - a.r0] = y;
-        } else {
-          int64_t addr;
-          int arr;
-          if (Pout.uniform) {
-            addr = Pout.col_off0 + row_offset_uniform(Pout, (uint32_t)row);
-            arr = Pout.uarray;
-          } else {
-            uint32_t idx[SMLRT_MAX_SWEEP];
-            unravel(Pout, (uint32_t)row, idx);
-            addr = col_address(Pout, 0, idx);
-            arr = __ldg(Pout.col_arr);
-          }
-          void* base = const_cast<void*>(dst.p[arr]);
-          if (dst.dt[arr] == SMLRT_F32)
-            reinterpret_cast<float*>(base)[addr] = y;
-          else
-            reinterpret_cast<double*>(base)[addr] = (double)y;
-        }
-      }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == WARP_MMA) {
-    tc_fence_after();
-    tmem_dealloc(tbase, 512);
-  }
-}
-
 // TS self-test: D[128 x N] = A[128 x K] * B[N x K]^T with A staged in TMEM by
-// tcgen05.st (bf16 pairs) exactly as the v2 epilogue stages activations.
+// tcgen05.st (bf16 pairs): validates the TMEM A-operand (TS) layout.
 template <int N>
 __global__ void __launch_bounds__(128, 1) tc_selftest_ts_kernel(const float* A, const float* B, int K, float* D) {
   extern __shared__ uint8_t smem_raw[];
@@ -898,33 +558,17 @@ int num_sms() {
   return n;
 }
 
-bool use_v2() {
-  static int v = -1;
-  if (v < 0) {
-    // v3 (TMEM A operand, two tiles in flight) is the default where the
-    // shape allows it; SMLRT_TC_VARIANT=v1 forces the SMEM-A2 kernel.
-    const char* e = getenv("SMLRT_TC_VARIANT");
-    v = (e != nullptr && e[0] == 'v' && e[1] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <int H1, int H2>
 int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
            int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
            int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   using L = Lay<H1, H2>;
-  constexpr bool v3_ok = (H1 == 256 && H2 <= H1 / 2);
-  const bool v3 = use_v2() && v3_ok;
   if (n_in > 8 || n_out > 8) return SMLRT_E_UNSUPPORTED;
   static int configured_mask = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured_mask & (1 << dev))) {
     SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC));
-    if constexpr (v3_ok)
-      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_v3_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      LayV3<H1, H2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
@@ -954,13 +598,6 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
   const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-  if constexpr (v3_ok) {
-    if (v3) {
-      mlp3_v3_kernel<H1, H2><<<grid, NTHREADS, LayV3<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
-      SMLRT_CUDA(cudaGetLastError());
-      return SMLRT_OK;
-    }
-  }
   mlp3_tc_kernel<H1, H2><<<grid, NTHREADS, L::ALLOC, s>>>(a, in, src, out, dst);
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
