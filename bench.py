@@ -142,8 +142,15 @@ def _cpu_worker(args):
         f"map(to: f({t.array}[{lo}:{hi}:{s0.step}" + "".join(f", {s}" for s in t.slices[1:]) + "]))").targets[0]
     st = lambda a: tuple(int(np.prod(a.shape[k + 1:])) for k in range(a.ndim))  # noqa: E731
     t0 = time.perf_counter()
-    oracle.region([(fi, sub(ti), src.reshape(-1), src.shape, st(src))],
-                  [(fo, sub(to), dst.reshape(-1), dst.shape, st(dst))], wl.layers)
+    if name == "particlefilter":
+        # the reference expresses the CNN as patch functor + infer + numpy pool
+        # + infer; cnn_forward restates exactly that
+        x = oracle.gather(fi, sub(ti), src.reshape(-1), src.shape, st(src)).reshape(r1 - r0, -1)
+        y, _ = oracle.cnn_forward(wl.layers, x, (1, 128, 128))
+        oracle.scatter(fo, sub(to), y, dst.reshape(-1), dst.shape, st(dst))
+    else:
+        oracle.region([(fi, sub(ti), src.reshape(-1), src.shape, st(src))],
+                      [(fo, sub(to), dst.reshape(-1), dst.shape, st(dst))], wl.layers)
     return time.perf_counter() - t0, (r1 - r0) * _inner_rows(wl)
 
 
@@ -154,7 +161,8 @@ def _inner_rows(wl):
 
 # CPU sample per config (first sweep rows): a few seconds of reference-path
 # work over all host cores; full size for C1 and C5
-CPU_SAMPLE = {"options": 1_000_000, "bonds": 262_144, "minibude": 16_384, "miniweather": 4094 * 2046}
+CPU_SAMPLE = {"options": 1_000_000, "bonds": 262_144, "minibude": 16_384, "miniweather": 4094 * 2046,
+              "particlefilter": 2_048}
 
 
 def _cpu_sample_elems(name):

@@ -90,12 +90,23 @@ typedef struct {
   int64_t row_pitch;   /* dense_rows: element step between rows (1-D)  */
 } smlrt_plan_info_t;
 
-/* A dense layer, host pointers, reference layout [out x in] row-major
- * (models.py:40-64); copied at upload. */
+typedef enum { SMLRT_DENSE = 0, SMLRT_CONV2D = 1, SMLRT_MAXPOOL2D = 2 } smlrt_layer_kind_t;
+
+/* One layer, host pointers, copied at upload.
+ *  DENSE    : weights [out x in] row-major + bias [out] (models.py:40-64).
+ *  CONV2D   : non-overlapping (stride == kernel) convolution of an
+ *             [in_channels x in_h x in_w] image; weights [out_channels x
+ *             in_channels*kernel*kernel] in (c, dy, dx) row-major order, bias
+ *             [out_channels]; out = out_channels*(in_h/k)*(in_w/k) flattened
+ *             (channel, row, column).  Format extension, SURVEY.md 8(f).
+ *  MAXPOOL2D: kernel x kernel max (NaN-propagating), no parameters.
+ * `in`/`out` are the flattened widths for every kind. */
 typedef struct {
+  int32_t kind;       /* smlrt_layer_kind_t */
   int32_t in;
   int32_t out;
   int32_t activation; /* smlrt_act_t */
+  int32_t kernel, stride, in_channels, in_h, in_w;
   const float* weights;
   const float* bias;
 } smlrt_layer_t;
@@ -129,7 +140,7 @@ int smlrt_model_upload(const smlrt_layer_t* layers, int n_layers,
                        int precision, int device, smlrt_model_t* out);
 int smlrt_model_free(smlrt_model_t model);
 /* which kernel region_infer would run: 0 none, 1 fused exact (templated),
- * 2 unfused exact, 3 fused tcgen05 bf16 */
+ * 2 unfused exact, 3 fused tcgen05 bf16, 4 fused conv front + exact dense */
 int smlrt_model_path(smlrt_model_t model, int32_t n_in_cols, int32_t* path);
 
 /* gather_batch / concretize_to (bridge.py:388-395, 457-462): rows

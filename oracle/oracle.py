@@ -158,3 +158,37 @@ def init_mlp_f32(dims, activation="relu", seed=0, bias_seed=1, bias_std=0.1):
 
 def dense_relu_model(dims, seed=0):
     return init_mlp_f32(dims, "relu", seed)
+
+
+def conv2d_patches(images, weights, bias, kernel, act):
+    """conv2d (stride == kernel) as the reference expresses it: the patch
+    functor [n, i, j, 0:k, 0:k] = ([n, i:i+k, j:j+k]) gathered by
+    concretize_to (bridge.py:388-395) fed to a dense layer via infer
+    (models.py:197-224).  images [N, C, H, W] -> [N, OC, H/k, W/k]."""
+    n, c, h, w = images.shape
+    k = kernel
+    oh, ow = h // k, w // k
+    patches = images.reshape(n, c, oh, k, ow, k).transpose(0, 2, 4, 1, 3, 5).reshape(n * oh * ow, c * k * k)
+    y, _ = infer([(weights, bias, act)], patches)
+    return y.reshape(n, oh, ow, -1).transpose(0, 3, 1, 2)
+
+
+def maxpool2d(x, k):
+    """k x k max pooling, NaN-propagating (np.max), [N, C, H, W]."""
+    n, c, h, w = x.shape
+    return x.reshape(n, c, h // k, k, w // k, k).max(axis=(3, 5))
+
+
+def cnn_forward(layers, x, input_shape):
+    """layers: [("conv2d", W, b, k, act) | ("maxpool2d", k) | ("dense", W, b, act)];
+    x [N, C*H*W] -> (y [N, G], finite).  Flattening is (channel, row, col)."""
+    h = np.asarray(x, dtype=np.float32).reshape((-1,) + tuple(input_shape))
+    for L in layers:
+        if L[0] == "conv2d":
+            h = conv2d_patches(h, L[1], L[2], L[3], L[4])
+        elif L[0] == "maxpool2d":
+            h = maxpool2d(h, L[1])
+        else:
+            h, _ = infer([(L[1], L[2], L[3])], h.reshape(h.shape[0], -1))
+    y = h.reshape(h.shape[0], -1)
+    return y, bool(np.isfinite(y).all())

@@ -51,12 +51,21 @@ class PlanInfo(C.Structure):
 
 class Layer(C.Structure):
     _fields_ = [
+        ("kind", C.c_int32),
         ("in_", C.c_int32),
         ("out", C.c_int32),
         ("activation", C.c_int32),
+        ("kernel", C.c_int32),
+        ("stride", C.c_int32),
+        ("in_channels", C.c_int32),
+        ("in_h", C.c_int32),
+        ("in_w", C.c_int32),
         ("weights", C.c_void_p),
         ("bias", C.c_void_p),
     ]
+
+
+KIND = {"dense": 0, "conv2d": 1, "maxpool2d": 2}
 
 
 _P = C.c_void_p
@@ -182,17 +191,30 @@ def plan_destroy(handle):
 # ----------------------------------------------------------------- models --
 
 def model_upload(layers, precision: int, device: int):
-    """layers: [(W float32 [out,in] contiguous ndarray, b float32 [out], act str)]."""
+    """layers: [(kind, W, b, act, params)] from Model.native_layers() (or the
+    legacy dense triples (W, b, act))."""
     L = lib()
     arr = (Layer * len(layers))()
     keep = []
-    for i, (w, b, act) in enumerate(layers):
-        keep += [w, b]
-        arr[i].in_ = w.shape[1]
-        arr[i].out = w.shape[0]
+    width = None
+    for i, spec in enumerate(layers):
+        if len(spec) == 3:
+            spec = ("dense", spec[0], spec[1], spec[2], {})
+        kind, w, b, act, prm = spec
+        arr[i].kind = KIND[kind]
         arr[i].activation = ACT[act]
-        arr[i].weights = w.ctypes.data
-        arr[i].bias = b.ctypes.data
+        if kind == "dense":
+            arr[i].in_, arr[i].out = w.shape[1], w.shape[0]
+        else:
+            c, h, wd, k = prm["in_channels"], prm["in_h"], prm["in_w"], prm["kernel"]
+            arr[i].kernel, arr[i].stride = k, prm["stride"]
+            arr[i].in_channels, arr[i].in_h, arr[i].in_w = c, h, wd
+            oc = w.shape[0] if kind == "conv2d" else c
+            arr[i].in_, arr[i].out = c * h * wd, oc * (h // k) * (wd // k)
+        if w is not None:
+            keep += [w, b]
+            arr[i].weights = w.ctypes.data
+            arr[i].bias = b.ctypes.data
     h = C.c_void_p()
     _check(L.smlrt_model_upload(arr, len(layers), precision, device, C.byref(h)))
     return h

@@ -60,12 +60,22 @@ extern "C" int smlrt_model_upload(const smlrt_layer_t* layers, int n_layers, int
     return fail(SMLRT_E_INVALID, "model_upload: unknown precision");
   for (int l = 0; l < n_layers; ++l) {
     const auto& L = layers[l];
-    if (L.in < 1 || L.out < 1 || !L.weights || !L.bias)
+    if (L.kind < SMLRT_DENSE || L.kind > SMLRT_MAXPOOL2D)
+      return fail(SMLRT_E_INVALID, "model_upload: unknown layer kind");
+    if (L.in < 1 || L.out < 1 || (L.kind != SMLRT_MAXPOOL2D && (!L.weights || !L.bias)))
       return fail(SMLRT_E_INVALID, "model_upload: empty layer " + std::to_string(l));
     if (L.activation < SMLRT_IDENTITY || L.activation > SMLRT_TANH)
       return fail(SMLRT_E_INVALID, "model_upload: unknown activation");
     if (l && L.in != layers[l - 1].out)
       return fail(SMLRT_E_MODEL_SHAPE, "model_upload: layer chain breaks at " + std::to_string(l));
+    if (L.kind != SMLRT_DENSE) {
+      const int k = L.kernel;
+      if (k < 1 || L.stride != k || L.in_channels < 1 || L.in_h % k || L.in_w % k ||
+          L.in != L.in_channels * L.in_h * L.in_w)
+        return fail(SMLRT_E_MODEL_SHAPE, "model_upload: bad conv/pool geometry at layer " + std::to_string(l));
+      if (L.out % ((L.in_h / k) * (L.in_w / k)))
+        return fail(SMLRT_E_MODEL_SHAPE, "model_upload: bad conv/pool output width at layer " + std::to_string(l));
+    }
   }
   int prev = 0;
   SMLRT_CUDA(cudaGetDevice(&prev));
@@ -80,14 +90,33 @@ extern "C" int smlrt_model_upload(const smlrt_layer_t* layers, int n_layers, int
   for (int l = 0; l < n_layers; ++l) {
     const auto& L = layers[l];
     DevLayer d;
+    d.kind = L.kind;
     d.in = L.in;
     d.out = L.out;
     d.act = L.activation;
-    size_t nw = (size_t)L.in * L.out;
+    d.kernel = L.kernel;
+    d.stride = L.stride;
+    d.in_c = L.in_channels;
+    d.in_h = L.in_h;
+    d.in_w = L.in_w;
     m->max_width = std::max(m->max_width, std::max(L.in, L.out));
-    if (cudaMalloc(&d.w, nw * 4) != cudaSuccess || cudaMalloc(&d.b, (size_t)L.out * 4) != cudaSuccess ||
+    if (L.kind == SMLRT_MAXPOOL2D) {
+      d.out_c = L.in_channels;
+      m->layers.push_back(d);
+      continue;
+    }
+    size_t nw, nb;
+    if (L.kind == SMLRT_CONV2D) {
+      d.out_c = L.out / ((L.in_h / L.kernel) * (L.in_w / L.kernel));
+      nw = (size_t)d.out_c * L.in_channels * L.kernel * L.kernel;
+      nb = (size_t)d.out_c;
+    } else {
+      nw = (size_t)L.in * L.out;
+      nb = (size_t)L.out;
+    }
+    if (cudaMalloc(&d.w, nw * 4) != cudaSuccess || cudaMalloc(&d.b, nb * 4) != cudaSuccess ||
         cudaMemcpy(d.w, L.weights, nw * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d.b, L.bias, (size_t)L.out * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(d.b, L.bias, nb * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
       m->layers.push_back(d);
       delete m;
       cudaSetDevice(prev);
@@ -95,7 +124,7 @@ extern "C" int smlrt_model_upload(const smlrt_layer_t* layers, int n_layers, int
     }
     m->layers.push_back(d);
     m->host_params.insert(m->host_params.end(), L.weights, L.weights + nw);
-    m->host_params.insert(m->host_params.end(), L.bias, L.bias + L.out);
+    m->host_params.insert(m->host_params.end(), L.bias, L.bias + nb);
   }
   if (precision == SMLRT_BF16) {
     int rc = tc_pack_model(*m);
@@ -121,7 +150,9 @@ extern "C" int smlrt_model_path(smlrt_model_t m, int32_t n_in_cols, int32_t* pat
   (void)n_in_cols;
   DevPlan dummy{};
   *path = 2;
-  if (m->precision == SMLRT_BF16) {
+  if (cnn_model(*m)) {
+    *path = 4;
+  } else if (m->precision == SMLRT_BF16) {
     if (launch_region_tc(*m, dummy, nullptr, nullptr, 0, dummy, nullptr, nullptr, 0, 0, 0, nullptr,
                          0, nullptr, true) == SMLRT_OK)
       *path = 3;
@@ -163,7 +194,7 @@ int forward_unfused(const smlrt_model_s& m, const float* x, int64_t rows, float*
   for (int l = 0; l < m.n_layers; ++l) {
     bool last = l == m.n_layers - 1;
     float* dst = last ? y : (l % 2 ? t1 : t0);
-    if (int rc = launch_dense_exact(cur, rows, m.layers[l], dst, s, last ? status : nullptr)) return rc;
+    if (int rc = launch_dense_exact_tiled(cur, rows, m.layers[l], dst, s, last ? status : nullptr)) return rc;
     cur = dst;
   }
   return SMLRT_OK;
@@ -178,7 +209,7 @@ extern "C" int smlrt_infer(smlrt_model_t m, const void* x, int32_t x_dtype, int6
   if (!m || !x || !y || !status) return fail(SMLRT_E_INVALID, "infer: null argument");
   if (rows <= 0) return SMLRT_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  int64_t ch = std::min(rows, kChunk);
+  int64_t ch = std::min(rows, cnn_model(*m) ? (int64_t)4096 : kChunk);
   Scratch sc(s);
   size_t per = (size_t)m->in_features + 2 * (size_t)m->max_width + m->out_features;
   if (int rc = sc.alloc(per * ch * 4)) return rc;
@@ -191,7 +222,11 @@ extern "C" int smlrt_infer(smlrt_model_t m, const void* x, int32_t x_dtype, int6
     int64_t n = std::min(ch, rows - r);
     const char* xp = (const char*)x + r * m->in_features * xs;
     if (int rc = launch_convert(xp, x_dtype, xin, SMLRT_F32, n * m->in_features, s)) return rc;
-    if (int rc = forward_unfused(*m, xin, n, yo, t0, t1, s, status)) return rc;
+    if (cnn_model(*m)) {
+      if (int rc = infer_cnn_dense(*m, xin, n, yo, s, status)) return rc;
+    } else if (int rc = forward_unfused(*m, xin, n, yo, t0, t1, s, status)) {
+      return rc;
+    }
     char* yp = (char*)y + r * m->out_features * ys;
     if (int rc = launch_convert(yo, SMLRT_F32, yp, y_dtype, n * m->out_features, s)) return rc;
   }
@@ -247,7 +282,12 @@ extern "C" int smlrt_region_infer(smlrt_plan_t pin, const void* const* in_ptrs, 
     }
   }
   int rc = SMLRT_E_UNSUPPORTED;
-  if (!(flags & SMLRT_FORCE_UNFUSED)) {
+  if (cnn_model(*m)) {
+    if (int e = launch_region_cnn(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt, pout->n_arrays,
+                                  r0, r1, staged, s, status))
+      return e;
+    rc = SMLRT_OK;
+  } else if (!(flags & SMLRT_FORCE_UNFUSED)) {
     if (m->precision == SMLRT_BF16)
       rc = launch_region_tc(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt,
                             pout->n_arrays, r0, r1, staged, s, status, false);

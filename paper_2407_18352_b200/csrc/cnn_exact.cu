@@ -1,0 +1,297 @@
+// Exact-fp32 CUDA-core kernels for the CNN surrogates and wide dense layers.
+//
+//   conv_front_kernel  : window gather (through the in-plan, or a dense batch)
+//                        -> non-overlapping conv2d -> act -> optional maxpool2d,
+//                        one CTA per sweep row (frame); the conv is the
+//                        reference's patch functor + dense layer, so every
+//                        output accumulates over (c, dy, dx) in row-major
+//                        order with separate RN multiply and add (bitwise
+//                        equal to _matmul_rowwise, models.py:188-194).
+//   dense_tiled_kernel : Y = act(X W^T + b), 64x64 output tile per CTA, K
+//                        staged through shared memory in chunks of 32; each
+//                        output still accumulates over the input index in
+//                        ascending order with separate multiply and add.
+// The C4 ParticleFilter config (conv 8x8/8 1->8, relu, maxpool 2, 512->128
+// relu, 128->2) runs as front kernel + two tiled dense layers + scatter.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace smlrt {
+namespace {
+
+__device__ __forceinline__ float act_exact(float y, int act) {
+  if (act == SMLRT_RELU) return (y < 0.0f) ? 0.0f : y;
+  if (act == SMLRT_TANH) return tanhf(y);
+  return y;
+}
+
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+struct FrontArgs {
+  // input addressing: either a dense batch (x != nullptr, row pitch in_feat)
+  // or the in-plan (uniform 2-D window fast path when win_w > 0)
+  const float* x;
+  int64_t r0, r1;
+  int C, H, W, K, OC, OH, OW;  // conv geometry
+  int act;
+  int pool;                    // maxpool kernel (1 = none)
+  int out_w;                   // floats per output row
+  const float* w;              // [OC][C*K*K]
+  const float* b;              // [OC]
+  float* out;                  // [rows][out_w]
+  const void* src;             // plan array base (window path)
+  int src_dt;
+};
+
+constexpr int kMaxOC = 16;
+
+__global__ void __launch_bounds__(256) conv_front_kernel(const __grid_constant__ FrontArgs a,
+                                                         const __grid_constant__ DevPlan P) {
+  extern __shared__ float sm[];
+  const int KK = a.C * a.K * a.K;
+  float* ws = sm;                          // [KK][OC] (transposed: o fastest)
+  float* conv = sm + KK * a.OC;            // [OC][OH][OW]
+  for (int i = threadIdx.x; i < KK * a.OC; i += blockDim.x) {
+    const int f = i / a.OC, o = i % a.OC;
+    ws[i] = a.w[o * KK + f];
+  }
+  __syncthreads();
+  const int64_t row = a.r0 + blockIdx.x;
+  int64_t base = 0;
+  if (a.x == nullptr) base = P.col_off0 + row_offset_uniform(P, (uint32_t)row);
+  const int npos = a.OH * a.OW;
+  for (int p = threadIdx.x; p < npos; p += blockDim.x) {
+    const int py = p / a.OW, px = p % a.OW;
+    float acc[kMaxOC];
+#pragma unroll
+    for (int o = 0; o < kMaxOC; ++o) acc[o] = 0.0f;
+    int f = 0;
+    for (int c = 0; c < a.C; ++c)
+      for (int dy = 0; dy < a.K; ++dy) {
+        const int y = py * a.K + dy;
+        for (int dx = 0; dx < a.K; ++dx, ++f) {
+          const int xx = px * a.K + dx;
+          const int64_t col = ((int64_t)c * a.H + y) * a.W + xx;  // flattened image index
+          float v;
+          if (a.x != nullptr) {
+            v = __ldg(a.x + (row - a.r0) * (int64_t)a.C * a.H * a.W + col);
+          } else if (P.win_w > 0 && a.C == 1) {
+            const int64_t addr = base + (int64_t)y * P.win_pitch + xx;
+            v = a.src_dt == SMLRT_F32 ? __ldg(reinterpret_cast<const float*>(a.src) + addr)
+                                      : __double2float_rn(__ldg(reinterpret_cast<const double*>(a.src) + addr));
+          } else {
+            const int64_t addr = __ldg(P.col_off + col) - P.col_off0 + base;
+            v = a.src_dt == SMLRT_F32 ? __ldg(reinterpret_cast<const float*>(a.src) + addr)
+                                      : __double2float_rn(__ldg(reinterpret_cast<const double*>(a.src) + addr));
+          }
+          const float* wf = ws + f * a.OC;
+#pragma unroll
+          for (int o = 0; o < kMaxOC; ++o)
+            if (o < a.OC) acc[o] = __fadd_rn(acc[o], __fmul_rn(v, wf[o]));
+        }
+      }
+#pragma unroll
+    for (int o = 0; o < kMaxOC; ++o)
+      if (o < a.OC) conv[o * npos + p] = act_exact(__fadd_rn(acc[o], __ldg(a.b + o)), a.act);
+  }
+  __syncthreads();
+  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  if (a.pool <= 1) {
+    for (int i = threadIdx.x; i < a.OC * npos; i += blockDim.x) orow[i] = conv[i];
+    return;
+  }
+  const int PH = a.OH / a.pool, PW = a.OW / a.pool;
+  for (int i = threadIdx.x; i < a.OC * PH * PW; i += blockDim.x) {
+    const int o = i / (PH * PW), q = i % (PH * PW), qy = q / PW, qx = q % PW;
+    float m = conv[o * npos + (qy * a.pool) * a.OW + qx * a.pool];
+    for (int dy = 0; dy < a.pool; ++dy)
+      for (int dx = 0; dx < a.pool; ++dx)
+        m = max_nan(m, conv[o * npos + (qy * a.pool + dy) * a.OW + qx * a.pool + dx]);
+    orow[i] = m;
+  }
+}
+
+// ------------------------------------------------------------ tiled dense --
+constexpr int TR = 64, TJ = 64, TK = 32;
+
+__global__ void __launch_bounds__(256) dense_tiled_kernel(const float* __restrict__ x, int64_t rows, int in,
+                                                          int out, const float* __restrict__ W,
+                                                          const float* __restrict__ b, int act,
+                                                          float* __restrict__ y, uint32_t* status) {
+  __shared__ float xs[TK][TR + 4];
+  __shared__ float wsh[TK][TJ + 4];
+  const int tr = threadIdx.x / 16, tj = threadIdx.x % 16;  // 16 x 16 threads, 4 x 4 outputs each
+  const int64_t row0 = (int64_t)blockIdx.x * TR;
+  const int j0 = blockIdx.y * TJ;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  for (int k0 = 0; k0 < in; k0 += TK) {
+    const int kn = min(TK, in - k0);
+    for (int i = threadIdx.x; i < TR * TK; i += 256) {
+      const int r = i / TK, k = i % TK;
+      const int64_t gr = row0 + r;
+      xs[k][r] = (gr < rows && k < kn) ? x[gr * in + k0 + k] : 0.0f;
+    }
+    for (int i = threadIdx.x; i < TJ * TK; i += 256) {
+      const int j = i / TK, k = i % TK;
+      wsh[k][j] = (j0 + j < out && k < kn) ? __ldg(W + (int64_t)(j0 + j) * in + k0 + k) : 0.0f;
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; ++k) {
+      const float4 xv = *reinterpret_cast<const float4*>(&xs[k][tr * 4]);
+      const float4 wv = *reinterpret_cast<const float4*>(&wsh[k][tj * 4]);
+      const float xr[4] = {xv.x, xv.y, xv.z, xv.w};
+      const float wr[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(xr[i], wr[j]));
+    }
+    __syncthreads();
+  }
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = row0 + tr * 4 + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = j0 + tj * 4 + j;
+      if (r < rows && c < out) {
+        const float v = act_exact(__fadd_rn(acc[i][j], __ldg(b + c)), act);
+        y[r * out + c] = v;
+        bad |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+      }
+    }
+  }
+  if (status != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(status, SMLRT_STATUS_NONFINITE);
+}
+
+int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const void* src, int src_dt,
+                 int64_t r0, int64_t r1, float* out, int* out_w, int* next_layer, cudaStream_t s) {
+  const DevLayer& c = m.layers[0];
+  FrontArgs a{};
+  a.x = x;
+  a.r0 = r0;
+  a.r1 = r1;
+  a.C = c.in_c;
+  a.H = c.in_h;
+  a.W = c.in_w;
+  a.K = c.kernel;
+  a.OC = c.out_c;
+  a.OH = c.in_h / c.kernel;
+  a.OW = c.in_w / c.kernel;
+  a.act = c.act;
+  a.w = c.w;
+  a.b = c.b;
+  a.out = out;
+  a.src = src;
+  a.src_dt = src_dt;
+  a.pool = 1;
+  *next_layer = 1;
+  if (m.n_layers > 1 && m.layers[1].kind == SMLRT_MAXPOOL2D) {
+    a.pool = m.layers[1].kernel;
+    *next_layer = 2;
+  }
+  a.out_w = m.layers[*next_layer - 1].out;
+  *out_w = a.out_w;
+  if (a.OC > kMaxOC) return fail(SMLRT_E_UNSUPPORTED, "conv2d with more than 16 output channels");
+  const size_t smem = ((size_t)a.C * a.K * a.K * a.OC + (size_t)a.OC * a.OH * a.OW) * 4;
+  if (smem > 200 * 1024) return fail(SMLRT_E_UNSUPPORTED, "conv2d front does not fit shared memory");
+  static int configured = 0;
+  if (!configured) {
+    SMLRT_CUDA(cudaFuncSetAttribute(conv_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = 1;
+  }
+  DevPlan dummy{};
+  conv_front_kernel<<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
+  SMLRT_CUDA(cudaGetLastError());
+  return SMLRT_OK;
+}
+
+// dense tail (layers [first, n)) over front output; ping-pong through t0/t1
+int dense_tail(const smlrt_model_s& m, int first, const float* cur, int64_t rows, float* y, float* t0, float* t1,
+               cudaStream_t s, uint32_t* status) {
+  for (int l = first; l < m.n_layers; ++l) {
+    const bool last = l == m.n_layers - 1;
+    float* dst = last ? y : ((l - first) % 2 ? t1 : t0);
+    if (int rc = launch_dense_exact_tiled(cur, rows, m.layers[l], dst, s, last ? status : nullptr)) return rc;
+    cur = dst;
+  }
+  return SMLRT_OK;
+}
+
+}  // namespace
+
+bool cnn_model(const smlrt_model_s& m) {
+  if (m.n_layers < 1 || m.layers[0].kind != SMLRT_CONV2D) return false;
+  int l = (m.n_layers > 1 && m.layers[1].kind == SMLRT_MAXPOOL2D) ? 2 : 1;
+  for (; l < m.n_layers; ++l)
+    if (m.layers[l].kind != SMLRT_DENSE) return false;
+  return true;
+}
+
+int launch_dense_exact_tiled(const float* x, int64_t rows, const DevLayer& L, float* y, cudaStream_t s,
+                             uint32_t* status) {
+  if (rows <= 0) return SMLRT_OK;
+  if (L.kind != SMLRT_DENSE) return fail(SMLRT_E_UNSUPPORTED, "layer order not supported by the exact path");
+  dim3 grid((unsigned)((rows + TR - 1) / TR), (unsigned)((L.out + TJ - 1) / TJ));
+  dense_tiled_kernel<<<grid, 256, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status);
+  SMLRT_CUDA(cudaGetLastError());
+  return SMLRT_OK;
+}
+
+int infer_cnn_dense(const smlrt_model_s& m, const float* x, int64_t rows, float* y, cudaStream_t s,
+                    uint32_t* status) {
+  if (!cnn_model(m)) return fail(SMLRT_E_UNSUPPORTED, "model is not conv2d(+maxpool) + dense");
+  float *f, *t0, *t1;
+  const size_t per = (size_t)m.max_width;
+  SMLRT_CUDA(cudaMallocAsync(&f, per * rows * 4 * 3, s));
+  t0 = f + per * rows;
+  t1 = t0 + per * rows;
+  int ow, nl;
+  int rc = launch_front(m, x, nullptr, nullptr, SMLRT_F32, 0, rows, f, &ow, &nl, s);
+  if (!rc) rc = (nl < m.n_layers) ? dense_tail(m, nl, f, rows, y, t0, t1, s, status)
+                                  : fail(SMLRT_E_UNSUPPORTED, "CNN without a dense head");
+  cudaFreeAsync(f, s);
+  return rc;
+}
+
+int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
+                      int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
+                      int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
+  if (!in.uniform) return fail(SMLRT_E_UNSUPPORTED, "CNN region needs a single-array input map");
+  const int64_t rows = r1 - r0;
+  const int64_t ch = std::min<int64_t>(rows, 16384);
+  const size_t per = (size_t)m.max_width;
+  float *buf;
+  SMLRT_CUDA(cudaMallocAsync(&buf, (per * 3 + m.out_features) * ch * 4, s));
+  float* f = buf;
+  float* t0 = f + per * ch;
+  float* t1 = t0 + per * ch;
+  float* yo = t1 + per * ch;
+  int rc = SMLRT_OK;
+  for (int64_t r = r0; r < r1 && !rc; r += ch) {
+    const int64_t n = std::min(ch, r1 - r);
+    int ow, nl;
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, s);
+    if (rc) break;
+    float* ydst = staged ? staged + (r - r0) * m.out_features : yo;
+    rc = dense_tail(m, nl, f, n, ydst, t0, t1, s, status);
+    if (rc) break;
+    if (!staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
+  }
+  cudaFreeAsync(buf, s);
+  (void)n_in;
+  return rc;
+}
+
+}  // namespace smlrt

@@ -66,6 +66,8 @@ struct DevPlan {
   int32_t uarray;           // uniform: the single array index
   int32_t dense_rows;       // uniform, 1-D sweep, columns one contiguous run
   int64_t col_off0;         // col_off[0] (host copy, for launch-time decisions)
+  int32_t win_w;            // >0: columns form a 2-D window of rows of win_w
+  int64_t win_pitch;        //     elements at this pitch (uniform plans)
 };
 
 __host__ __device__ __forceinline__ int64_t row_offset_uniform(const DevPlan& p, uint32_t r) {
@@ -129,6 +131,8 @@ struct smlrt_plan_s {
   bool dense_rows = false;
   int64_t row_pitch = 0;
   bool injective = false;
+  int win_w = 0;
+  int64_t win_pitch = 0;
   std::mutex mu;
   std::map<int, smlrt::DeviceTables> dev;
   ~smlrt_plan_s();
@@ -140,7 +144,9 @@ namespace smlrt {
 
 // one dense layer on the device
 struct DevLayer {
+  int kind = SMLRT_DENSE;
   int in, out, act;
+  int kernel = 0, stride = 0, in_c = 0, in_h = 0, in_w = 0, out_c = 0;
   float* w = nullptr;       // f32 [out][in]
   float* b = nullptr;       // f32 [out]
   void* w_bf16 = nullptr;   // bf16 weights in the tcgen05 operand layout
@@ -178,6 +184,15 @@ int launch_region_exact_fused(const smlrt_model_s& m, const DevPlan& in, const v
                               void* const* out_ptrs, const int32_t* out_dt, int n_out,
                               int64_t r0, int64_t r1, float* staged, cudaStream_t s,
                               uint32_t* status, bool probe_only);
+// conv2d(+maxpool2d) front + exact dense tail (cnn_exact.cu)
+bool cnn_model(const smlrt_model_s& m);
+int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
+                      int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
+                      int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
+int infer_cnn_dense(const smlrt_model_s& m, const float* x, int64_t rows, float* y, cudaStream_t s,
+                    uint32_t* status);
+int launch_dense_exact_tiled(const float* x, int64_t rows, const DevLayer& L, float* y, cudaStream_t s,
+                             uint32_t* status);
 int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
                      const int32_t* in_dt, int n_in, const DevPlan& out, void* const* out_ptrs,
                      const int32_t* out_dt, int n_out, int64_t r0, int64_t r1, float* staged,

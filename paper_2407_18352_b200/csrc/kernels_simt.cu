@@ -329,7 +329,7 @@ bool dims_match(const smlrt_model_s& m) {
   constexpr int n = sizeof...(D);
   if (m.n_layers != n - 1) return false;
   for (int l = 0; l < m.n_layers; ++l)
-    if (m.layers[l].in != d[l] || m.layers[l].out != d[l + 1]) return false;
+    if (m.layers[l].kind != SMLRT_DENSE || m.layers[l].in != d[l] || m.layers[l].out != d[l + 1]) return false;
   return true;
 }
 

@@ -547,6 +547,8 @@ std::vector<uint8_t> pack(const smlrt_model_s& m) {
 }
 
 bool shape_is(const smlrt_model_s& m, int h1, int h2) {
+  for (const auto& L : m.layers)
+    if (L.kind != SMLRT_DENSE) return false;
   return m.n_layers == 3 && m.in_features <= KX && m.layers[0].out == h1 && m.layers[1].out == h2 &&
          m.layers[2].out == 1;
 }

@@ -91,6 +91,8 @@ int smlrt_plan_s::tables(DevPlan* p) {
   p->cdiv = FastDiv((uint32_t)n_cols);
   p->dense_rows = dense_rows;
   p->col_off0 = col_off.empty() ? 0 : col_off[0];
+  p->win_w = win_w;
+  p->win_pitch = win_pitch;
   p->col_off = it->second.col_off;
   p->col_arr = it->second.col_arr;
   p->col_str = it->second.col_str;
@@ -194,6 +196,12 @@ extern "C" int smlrt_plan_create(const smlrt_view_t* views, int n_views, int n_s
       if (p->col_off[c] != p->col_off[0] + c) run = false;
     p->dense_rows = run && n_sweep == 1;
     p->row_pitch = p->dense_rows ? p->ustride[0] : 0;
+  }
+
+  // ---- 2-D window detection (one view, two feature axes, inner stride 1) ----
+  if (p->uniform && n_views == 1 && views[0].n_feat == 2 && views[0].feat_stride[1] == 1) {
+    p->win_w = (int)views[0].feat_count[1];
+    p->win_pitch = views[0].feat_stride[0];
   }
 
   // ---- injectivity (FROM) ----

@@ -18,7 +18,7 @@ import torch
 
 from .bridge import ArrayBuffer
 from .directives import parse_directive
-from .models import DenseLayer, Model
+from .models import Conv2dLayer, DenseLayer, MaxPool2dLayer, Model
 from .runtime import BoundMap, RegionDescriptor
 
 __all__ = ["CONFIGS", "Workload", "make", "init_weights"]
@@ -40,10 +40,11 @@ class Spec:
     bound: str          # roofline bound: "hbm" | "tensor" | "fp32"
     bytes_per_elem: int  # compulsory HBM bytes per element (section 8(d))
     notes: str = ""
+    flops: int = 0        # override for non-MLP models
 
     @property
     def flops_per_elem(self) -> int:
-        return 2 * sum(a * b for a, b in zip(self.dims, self.dims[1:]))
+        return self.flops or 2 * sum(a * b for a, b in zip(self.dims, self.dims[1:]))
 
 
 CONFIGS = {
@@ -56,6 +57,13 @@ CONFIGS = {
     "minibude": Spec("minibude", 67_108_864, [6, 1024, 512, 256, 1], "bf16",
                      "functor(pin: [p, 0:6] = ([0:6, p]))", "functor(pout: [p, 0:1] = ([p]))",
                      "map(to: pin(poses[0:N]))", "map(from: pout(energy[0:N]))", "tensor", 28),
+    # conv 8x8/8 1->8 relu, maxpool 2, FC 512->128 relu, FC 128->2 (Table IV PF);
+    # flops 2*(256*8*64 + 512*128 + 128*2) = 393,728; bytes 128*128*4 + 2*4
+    "particlefilter": Spec("particlefilter", 16_384, [16384, 512, 128, 2], "fp32",
+                           "functor(win: [k, 0:128, 0:128] = ([k, 16:144, 16:144]))",
+                           "functor(loc: [k, 0:2] = ([k, 0], [k, 1]))",
+                           "map(to: win(frames[0:N]))", "map(from: loc(locs[0:N]))", "hbm", 65_544,
+                           flops=393_728),
     "miniweather": Spec("miniweather", 4094 * 2046, [36, 8, 4], "fp32",
                         "functor(halo: [i, j, 0:4, 0:3, 0:3] = ([0:4, i-1:i+2, j-1:j+2]))",
                         "functor(pts: [i, j, 0:4] = ([0, i, j], [1, i, j], [2, i, j], [3, i, j]))",
@@ -125,11 +133,24 @@ class Workload:
             out_maps=[BoundMap(fo, to, self.buffers[out_name])], env=self.env)
 
 
+def cnn_layers(seed=0):
+    """ParticleFilter CNN weights: conv as a 64->8 dense (He init), FC 512-128-2."""
+    (cw, cb, _), _ = init_weights([64, 8, 8], seed=seed)
+    fc = init_weights([512, 128, 2], seed=seed + 1)
+    return [("conv2d", cw, cb, 8, "relu"), ("maxpool2d", 2)] + [("dense", w, b, a) for w, b, a in fc]
+
+
 def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Workload:
     s = CONFIGS[name]
-    layers = init_weights(s.dims)
-    model = Model(s.dims[0], s.dims[-1], [DenseLayer(w, b, a) for w, b, a in layers],
-                  precision=s.precision)
+    if name == "particlefilter":
+        layers = cnn_layers()
+        model = Model(16384, 2, [Conv2dLayer(layers[0][1], layers[0][2], 8, 8, "relu"),
+                                 MaxPool2dLayer(2)] + [DenseLayer(w, b, a) for _, w, b, a in layers[2:]],
+                      precision="fp32", input_shape=(1, 128, 128))
+    else:
+        layers = init_weights(s.dims)
+        model = Model(s.dims[0], s.dims[-1], [DenseLayer(w, b, a) for w, b, a in layers],
+                      precision=s.precision)
     if name == "options":
         n = elements or s.elements
         rng = np.random.default_rng(0 + seed_offset)
@@ -145,6 +166,11 @@ def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Worklo
         rng = np.random.default_rng(3 + seed_offset)
         poses = (rng.random((6, n), dtype=np.float32) * 2 - 1).astype(np.float32)
         arrays, env = {"poses": poses, "energy": np.zeros(n, np.float32)}, {"N": n}
+    elif name == "particlefilter":
+        n = elements or s.elements
+        rng = np.random.default_rng(4 + seed_offset)
+        arrays = {"frames": rng.random((n, 160, 160), dtype=np.float32), "locs": np.zeros((n, 2), np.float32)}
+        env = {"N": n}
     elif name == "miniweather":
         nx, nz = (4096, 2048) if elements is None else _grid_for(elements)
         state = np.stack([_bumps(nx, nz, k + seed_offset) for k in range(4)])

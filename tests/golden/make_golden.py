@@ -237,6 +237,32 @@ with tempfile.TemporaryDirectory() as td:
         r["created_utc"] = "<nondeterministic>"
     meta["srdb_manifest"] = man
 
+# 7. CNN (ParticleFilter shape) composed from reference pieces (SURVEY.md
+#    section 8(c)): concretize_to with the 8x8 patch functor -> infer 64->8 relu
+#    -> numpy 2x2 maxpool -> infer 512->128 relu -> 128->2
+prng = np.random.default_rng(4)
+frames = prng.random((3, 160, 160), dtype=np.float32)
+m_conv = frozen([64, 8, 8])  # two layers; use the first (relu) as the conv
+conv_w, conv_b = m_conv.layers[0].weights, m_conv.layers[0].bias
+m_fc = frozen([512, 128, 2])
+patch = parse_directive("functor(pf: [f, i, j, 0:8, 0:8] = ([f, i:i+8, j:j+8]))")
+ptarget = parse_directive("map(to: pf(frames[0:3, 16:137:8, 16:137:8]))").targets[0]
+pt = concretize_to(patch, ptarget, ArrayBuffer.from_numpy(frames))          # (3, 16, 16, 8, 8)
+conv = infer(Model(64, 8, [DenseLayer(conv_w, conv_b, "relu")]), pt.data.reshape(-1, 64))
+conv = conv.reshape(3, 16, 16, 8).transpose(0, 3, 1, 2)                   # (n, c, y, x)
+pooled = conv.reshape(3, 8, 8, 2, 8, 2).max(axis=(3, 5)).reshape(3, 512)
+y = infer(m_fc, pooled)
+put("cnn_frames", frames)
+put("cnn_conv_w", conv_w)
+put("cnn_conv_b", conv_b)
+for k, L in enumerate(m_fc.layers):
+    put(f"cnn_fc_W{k}", L.weights)
+    put(f"cnn_fc_b{k}", L.bias)
+put("cnn_pooled", pooled)
+put("cnn_y", y)
+meta["cnn"] = {"window": "frames[k, 16:144, 16:144]", "conv": [1, 8, 8, 8], "pool": 2,
+               "fc": [512, 128, 2], "acts": ["relu", "relu", "identity"]}
+
 np.savez_compressed(OUT / "golden.npz", **arrays)
 (OUT / "golden.json").write_text(json.dumps(meta, indent=1) + "\n")
 print(f"wrote {len(arrays)} arrays, {len(meta['c1'])} c1 cases, {len(errs)} error cases")

@@ -46,3 +46,19 @@ def test_srdb_bytes_identical(tmp_path):
         recs = db.read_records("stencil")
         assert [r.elapsed_ns for r in recs] == [1000, 1001, 1002]
         assert np.array_equal(recs[1].inputs.to_numpy(), a["srdb_x1"])
+
+
+def test_cnn_model_v2_round_trip(tmp_path):
+    from paper_2407_18352_b200 import workloads
+    from paper_2407_18352_b200.models import Conv2dLayer, MaxPool2dLayer
+    m = workloads.make("particlefilter", 2).model
+    save_model(m, tmp_path / "pf")
+    man = json.loads((tmp_path / "pf" / "model.json").read_text())
+    assert man["version"] == 2 and man["input_shape"] == [1, 128, 128]
+    assert [L.get("kind") for L in man["layers"]] == ["conv2d", "maxpool2d", "dense", "dense"]
+    m2 = load_model(tmp_path / "pf")
+    assert isinstance(m2.layers[0], Conv2dLayer) and isinstance(m2.layers[1], MaxPool2dLayer)
+    assert m2.dims == [16384, 2048, 512, 128, 2]
+    for a_, b_ in zip(m.layers, m2.layers):
+        if hasattr(a_, "weights"):
+            assert a_.weights.tobytes() == b_.weights.tobytes()

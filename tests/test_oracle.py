@@ -126,3 +126,13 @@ def test_region_weather_golden():
     oracle.region([(fi, tg, state.reshape(-1), (4, 20, 24), (480, 24, 1))],
                   [(fo, tg, new, (4, 20, 24), (480, 24, 1))], layers)
     assert new.tobytes() == a["region_weather_new"].tobytes()
+
+
+def test_cnn_oracle_matches_reference_composition():
+    a = arrays()
+    layers = [("conv2d", a["cnn_conv_w"], a["cnn_conv_b"], 8, "relu"), ("maxpool2d", 2),
+              ("dense", a["cnn_fc_W0"], a["cnn_fc_b0"], "relu"),
+              ("dense", a["cnn_fc_W1"], a["cnn_fc_b1"], "identity")]
+    x = a["cnn_frames"][:, 16:144, 16:144].reshape(3, -1)
+    y, finite = oracle.cnn_forward(layers, x, (1, 128, 128))
+    assert finite and y.tobytes() == a["cnn_y"].tobytes()
