@@ -18,10 +18,24 @@ int device_tables(smlrt_plan_t p, DevPlan* d, const int32_t* dtypes, int n) {
   return SMLRT_OK;
 }
 
+// Keep the device's stream-ordered pool from returning memory at every
+// synchronisation, so per-call scratch is a pool hit after the first call.
+void warm_pool() {
+  static int done_mask = 0;
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || (done_mask & (1 << d))) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_mask |= 1 << d;
+}
+
 struct Scratch {  // stream-ordered temporary
   void* p = nullptr;
   cudaStream_t s;
-  explicit Scratch(cudaStream_t st) : s(st) {}
+  explicit Scratch(cudaStream_t st) : s(st) { warm_pool(); }
   int alloc(size_t bytes) {
     if (bytes == 0) return SMLRT_OK;
     SMLRT_CUDA(cudaMallocAsync(&p, bytes, s));
@@ -283,6 +297,7 @@ extern "C" int smlrt_region_infer(smlrt_plan_t pin, const void* const* in_ptrs, 
   }
   int rc = SMLRT_E_UNSUPPORTED;
   if (cnn_model(*m)) {
+    warm_pool();
     if (int e = launch_region_cnn(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt, pout->n_arrays,
                                   r0, r1, staged, s, status))
       return e;

@@ -116,6 +116,79 @@ __global__ void __launch_bounds__(256) conv_front_kernel(const __grid_constant__
   }
 }
 
+// Compile-time geometry (C = 1, K = 8, OC = 8: the C4 model): one thread per
+// conv position, each patch row fetched as two float4, weights as float4
+// broadcasts from shared memory; same (dy, dx) accumulation order.
+template <int K, int OC>
+__global__ void __launch_bounds__(256) conv_front_fixed_kernel(const __grid_constant__ FrontArgs a,
+                                                               const __grid_constant__ DevPlan P) {
+  static_assert(K % 4 == 0 && OC % 4 == 0, "vector widths");
+  extern __shared__ float sm[];
+  float* ws = sm;                 // [K*K][OC]
+  float* conv = sm + K * K * OC;  // [OC][OH][OW]
+  for (int i = threadIdx.x; i < K * K * OC; i += blockDim.x) ws[i] = a.w[(i % OC) * K * K + i / OC];
+  __syncthreads();
+  const int64_t row = a.r0 + blockIdx.x;
+  const float* img;
+  int64_t pitch;
+  if (a.x != nullptr) {
+    img = a.x + (row - a.r0) * (int64_t)a.H * a.W;
+    pitch = a.W;
+  } else {
+    img = reinterpret_cast<const float*>(a.src) + P.col_off0 + row_offset_uniform(P, (uint32_t)row);
+    pitch = P.win_pitch;
+  }
+  const int npos = a.OH * a.OW;
+  for (int p = threadIdx.x; p < npos; p += blockDim.x) {
+    const int py = p / a.OW, px = p % a.OW;
+    float acc[OC];
+#pragma unroll
+    for (int o = 0; o < OC; ++o) acc[o] = 0.0f;
+    const float* prow = img + (int64_t)(py * K) * pitch + px * K;
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy) {
+      float v[K];
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        const float4 u = __ldg(reinterpret_cast<const float4*>(prow + dy * pitch) + q);
+        v[4 * q] = u.x;
+        v[4 * q + 1] = u.y;
+        v[4 * q + 2] = u.z;
+        v[4 * q + 3] = u.w;
+      }
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx) {
+        const float* wf = ws + (dy * K + dx) * OC;
+#pragma unroll
+        for (int o4 = 0; o4 < OC / 4; ++o4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(wf + 4 * o4);
+          acc[4 * o4] = __fadd_rn(acc[4 * o4], __fmul_rn(v[dx], w4.x));
+          acc[4 * o4 + 1] = __fadd_rn(acc[4 * o4 + 1], __fmul_rn(v[dx], w4.y));
+          acc[4 * o4 + 2] = __fadd_rn(acc[4 * o4 + 2], __fmul_rn(v[dx], w4.z));
+          acc[4 * o4 + 3] = __fadd_rn(acc[4 * o4 + 3], __fmul_rn(v[dx], w4.w));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < OC; ++o) conv[o * npos + p] = act_exact(__fadd_rn(acc[o], __ldg(a.b + o)), a.act);
+  }
+  __syncthreads();
+  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  if (a.pool <= 1) {
+    for (int i = threadIdx.x; i < OC * npos; i += blockDim.x) orow[i] = conv[i];
+    return;
+  }
+  const int PH = a.OH / a.pool, PW = a.OW / a.pool;
+  for (int i = threadIdx.x; i < OC * PH * PW; i += blockDim.x) {
+    const int o = i / (PH * PW), q = i % (PH * PW), qy = q / PW, qx = q % PW;
+    float m = conv[o * npos + (qy * a.pool) * a.OW + qx * a.pool];
+    for (int dy = 0; dy < a.pool; ++dy)
+      for (int dx = 0; dx < a.pool; ++dx)
+        m = max_nan(m, conv[o * npos + (qy * a.pool + dy) * a.OW + qx * a.pool + dx]);
+    orow[i] = m;
+  }
+}
+
 // ------------------------------------------------------------ tiled dense --
 constexpr int TR = 64, TJ = 64, TK = 32;
 
@@ -212,7 +285,15 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
     configured = 1;
   }
   DevPlan dummy{};
-  conv_front_kernel<<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
+  const bool aligned = (a.x != nullptr && a.W % 4 == 0) ||
+                       (P != nullptr && src_dt == SMLRT_F32 && P->win_w == a.W && P->win_pitch % 4 == 0 &&
+                        ((P->col_off0 + P->ustride[0]) % 4 == 0) && P->n_sweep == 1 && P->col_off0 % 4 == 0 &&
+                        (reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned) {
+    conv_front_fixed_kernel<8, 8><<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
+  } else {
+    conv_front_kernel<<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
+  }
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -253,7 +334,8 @@ int infer_cnn_dense(const smlrt_model_s& m, const float* x, int64_t rows, float*
                     uint32_t* status) {
   if (!cnn_model(m)) return fail(SMLRT_E_UNSUPPORTED, "model is not conv2d(+maxpool) + dense");
   float *f, *t0, *t1;
-  const size_t per = (size_t)m.max_width;
+  size_t per = 1;
+  for (int l = 1; l < m.n_layers; ++l) per = std::max(per, (size_t)m.layers[l].out);
   SMLRT_CUDA(cudaMallocAsync(&f, per * rows * 4 * 3, s));
   t0 = f + per * rows;
   t1 = t0 + per * rows;
@@ -271,7 +353,8 @@ int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* con
   if (!in.uniform) return fail(SMLRT_E_UNSUPPORTED, "CNN region needs a single-array input map");
   const int64_t rows = r1 - r0;
   const int64_t ch = std::min<int64_t>(rows, 16384);
-  const size_t per = (size_t)m.max_width;
+  size_t per = 1;  // widest activation after the conv front
+  for (int l = 1; l < m.n_layers; ++l) per = std::max(per, (size_t)m.layers[l].out);
   float *buf;
   SMLRT_CUDA(cudaMallocAsync(&buf, (per * 3 + m.out_features) * ch * 4, s));
   float* f = buf;
