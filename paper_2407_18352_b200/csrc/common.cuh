@@ -198,5 +198,11 @@ int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* cons
                      const int32_t* out_dt, int n_out, int64_t r0, int64_t r1, float* staged,
                      cudaStream_t s, uint32_t* status, bool probe_only);
 int tc_pack_model(smlrt_model_s& m);
+// wide 4-layer MLPs (gemm_tc.cu): TMA-fed tcgen05 GEMM chain
+bool wide_shape(const smlrt_model_s& m);
+int wide_pack(smlrt_model_s& m);
+int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
+                       const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
+                       int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 
 }  // namespace smlrt

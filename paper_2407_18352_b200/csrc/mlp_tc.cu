@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(128, 1) tc_selftest_kernel(const float* A, con
 }  // namespace
 
 int tc_pack_model(smlrt_model_s& m) {
+  if (wide_shape(m)) return wide_pack(m);
   std::vector<uint8_t> blob;
   if (shape_is(m, 256, 128))
     blob = pack<256, 128>(m);
@@ -690,9 +691,11 @@ int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* cons
                      int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                      int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status, bool probe_only) {
   if (m.tc_blob == nullptr && !(probe_only && m.precision == SMLRT_BF16 &&
-                                (shape_is(m, 256, 128) || shape_is(m, 128, 64))))
+                                (shape_is(m, 256, 128) || shape_is(m, 128, 64) || wide_shape(m))))
     return SMLRT_E_UNSUPPORTED;
   if (probe_only) return SMLRT_OK;
+  if (wide_shape(m))
+    return launch_region_wide(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
   if (shape_is(m, 256, 128))
     return launch<256, 128>(m, in, in_ptrs, in_dt, n_in, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
   if (shape_is(m, 128, 64))
