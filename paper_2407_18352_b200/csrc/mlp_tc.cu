@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -41,22 +42,25 @@ constexpr int NTHREADS = 17 * 32;
 // 0 and 1 = 1.0) times a bias tile [N x 16] holding bf16(b) in k=0 and
 // bf16(b - bf16(b)) in k=1 adds b (to ~16 mantissa bits) to every row of the
 // accumulator, so the epilogues never touch the biases.
-template <int H1, int H2>
+template <int H1, int H2, int NS = 1>
 struct Lay {
+  // NS = 2: CTA-pair (cta_group::2) kernel -- every B operand (W1, W2 and the
+  // bias tiles) is split along N, each CTA holding rows [rank N/2, (rank+1) N/2)
   static_assert(H1 % 64 == 0 && H1 >= 64 && H1 <= 256, "H1: multiple of 64, <= 256");
   static_assert(H2 % 32 == 0 && H2 >= 32 && H2 <= 256, "H2: multiple of 32, <= 256");
   static_assert(H1 + 2 * H2 <= 512, "TMEM columns");
   static constexpr int KC = H1 / 64;          // layer-2 K chunks of 64
-  static constexpr int W2_CHUNK = H2 * 128;   // [H2][64] bf16, SW128
+  static constexpr int N1 = H1 / NS, N2 = H2 / NS;  // B rows held by this CTA
+  static constexpr int W2_CHUNK = N2 * 128;   // [N2][64] bf16, SW128
   static constexpr int A2_CHUNK = BM * 128;   // [128][64] bf16, SW128
   static constexpr int A2_BUF = KC * A2_CHUNK;
   static constexpr int X_STAGE = BM * 32;     // [128][16] bf16, SW32
   static constexpr int OFF_W2 = 0;
   static constexpr int OFF_A2 = OFF_W2 + KC * W2_CHUNK;
-  static constexpr int OFF_W1 = OFF_A2 + 2 * A2_BUF;   // [H1][16] SW32
-  static constexpr int OFF_W1B = OFF_W1 + H1 * 32;     // [H1][16] SW32 bias tile
-  static constexpr int OFF_W2B = OFF_W1B + H1 * 32;    // [H2][16] SW32 bias tile
-  static constexpr int OFF_ONES = OFF_W2B + H2 * 32;   // [128][16] SW32
+  static constexpr int OFF_W1 = OFF_A2 + 2 * A2_BUF;   // [N1][16] SW32
+  static constexpr int OFF_W1B = OFF_W1 + N1 * 32;     // [N1][16] SW32 bias tile
+  static constexpr int OFF_W2B = OFF_W1B + N1 * 32;    // [N2][16] SW32 bias tile
+  static constexpr int OFF_ONES = OFF_W2B + N2 * 32;   // [128][16] SW32
   static constexpr int OFF_X = OFF_ONES + BM * 32;
   static constexpr int OFF_W3 = OFF_X + XSTAGES * X_STAGE;
   static constexpr int OFF_B3 = OFF_W3 + H2 * 4;
@@ -78,9 +82,9 @@ struct Lay {
   static_assert(ALLOC <= 232448, "shared memory budget");
   // global blob produced by tc_pack_model: W2 | W1 | W1B | W2B | w3 | b3 (same order as smem)
   static constexpr int BLOB_W1 = KC * W2_CHUNK;
-  static constexpr int BLOB_TAIL = BLOB_W1 + 2 * H1 * 32 + H2 * 32;
+  static constexpr int BLOB_TAIL = BLOB_W1 + 2 * N1 * 32 + N2 * 32;
   static constexpr int TAIL = H2 * 4 + 16;
-  static constexpr int BLOB = BLOB_TAIL + TAIL;
+  static constexpr int BLOB = BLOB_TAIL + TAIL;  // per CTA rank; NS of them back to back
   static constexpr int T_L1 = 0, T_L2 = H1;  // TMEM column bases
 };
 
@@ -124,14 +128,48 @@ __device__ __forceinline__ float ld_elem(const void* base, int dt, int64_t i) {
                          : __double2float_rn(__ldg(reinterpret_cast<const double*>(base) + i));
 }
 
+// Debug-only pipeline trace (build with -DSMLRT_TC_TRACE; `make trace`):
+// clock64 stamps of each role's events for the first TR_TILES tiles of CTAs 0/1.
+#ifdef SMLRT_TC_TRACE
+constexpr int TR_TILES = 64, TR_EV = 16;
+__device__ unsigned long long g_tc_trace[2][TR_TILES][TR_EV];
+#define TR(ev, it)                                                   \
+  do {                                                               \
+    if (blockIdx.x < 2 && (it) < TR_TILES)                           \
+      g_tc_trace[blockIdx.x][(it)][(ev)] = clock64();                \
+  } while (0)
+#else
+#define TR(ev, it) \
+  do {             \
+  } while (0)
+#endif
+
+// Tile schedule: single CTAs take 128-row tiles blockIdx + i*grid; a CTA pair
+// takes 256-row pair tiles (cluster + i*clusters), rank r owning rows [128 r, 128 r + 128).
+struct Sched {
+  int first, stride, rank, pair;
+  __device__ __forceinline__ int64_t tile(int it) const {
+    const int64_t t = (int64_t)first + (int64_t)it * stride;
+    return pair ? 2 * t + rank : t;
+  }
+};
+
+// producers/consumers arrive on the MMA-issuing CTA's barrier (rank 0 of a pair)
+template <bool PAIR>
+__device__ __forceinline__ void arrive_mma(uint64_t* bar) {
+  if constexpr (PAIR)
+    mbar_arrive_cluster(mapa(bar, 0));
+  else
+    mbar_arrive(bar);
+}
+
 // ------------------------------------------------------------ epilogue 1
 // TMEM L1 accumulator (bias already added by the MMA) -> act -> bf16 ->
 // A2[b] in the SW128 K-major layout layer 2 consumes.  Thread = row r; this
 // warpgroup covers columns [half*H1/2, (half+1)*H1/2).
-template <int ACT, int H1, int H2>
+template <int ACT, int H1, int H2, class L, bool PAIR>
 __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int half,
                                           int q, int lane) {
-  using L = Lay<H1, H2>;
   constexpr int HC = H1 / 2;
   const int r = q * 32 + lane;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L1 + half * HC;
@@ -143,38 +181,45 @@ __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t
   for (int it = 0; it < n_my; ++it) {
     const int b = it & 1;
     mbar_wait(bar + L::B_L1FULL, it & 1);
-    mbar_wait(bar + L::B_A2EMPTY + b, ((it >> 1) & 1) ^ 1);
+    if (q == 0 && half == 0 && lane == 0) TR(2, it);
     tc_fence_after();
+    // x16 loads with the next one in flight while the current one is
+    // activated, packed and stored; the L1 buffer is released after the last load
+    mbar_wait(bar + L::B_A2EMPTY + b, ((it >> 1) & 1) ^ 1);
+    if (q == 0 && half == 0 && lane == 0) TR(3, it);
     const uint32_t boff = b * L::A2_BUF;
+    uint32_t v[2][16];
+    tmem_ld16(lane_addr, v[0]);
 #pragma unroll
-    for (int cc = 0; cc < HC / 32; ++cc) {
-      uint32_t v[32];
-      tmem_ld32(lane_addr + cc * 32, v);
-      tmem_wait_ld();
-      if (cc == HC / 32 - 1) {
+    for (int c = 0; c < HC / 16; ++c) {
+      tmem_wait_ld16(v[c & 1]);
+      if (c + 1 < HC / 16) {
+        tmem_ld16(lane_addr + (c + 1) * 16, v[(c + 1) & 1]);
+      } else {
         tc_fence_before();
-        mbar_arrive(bar + L::B_L1EMPTY);
+        arrive_mma<PAIR>(bar + L::B_L1EMPTY);
+        if (q == 0 && half == 0 && lane == 0) TR(4, it);
       }
-      const float* f = reinterpret_cast<const float*>(v);
-      const uint32_t coff = boff + (cc >> 1) * L::A2_CHUNK;
+      const float* f = reinterpret_cast<const float*>(v[c & 1]);
+      const uint32_t coff = boff + (c >> 2) * L::A2_CHUNK;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        st_shared_v4(xo[(cc & 1) * 4 + j] + coff, act_pack<ACT>(f[8 * j], f[8 * j + 1]),
+      for (int j = 0; j < 2; ++j)
+        st_shared_v4(xo[((c >> 1) & 1) * 4 + (c & 1) * 2 + j] + coff, act_pack<ACT>(f[8 * j], f[8 * j + 1]),
                      act_pack<ACT>(f[8 * j + 2], f[8 * j + 3]), act_pack<ACT>(f[8 * j + 4], f[8 * j + 5]),
                      act_pack<ACT>(f[8 * j + 6], f[8 * j + 7]));
     }
     fence_async_smem();
-    mbar_arrive(bar + L::B_A2FULL + b);
+    arrive_mma<PAIR>(bar + L::B_A2FULL + b);
+    if (q == 0 && half == 0 && lane == 0) TR(5, it);
   }
 }
 
 // ------------------------------------------------------------ epilogue 2
 // TMEM L2 accumulator (+b2 from the MMA) -> act -> dot w3 -> +b3 -> act3 ->
 // scatter.  Thread = row.
-template <int ACT, int H1, int H2>
+template <int ACT, int H1, int H2, class L, bool PAIR>
 __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int q, int lane,
-                                          const TcArgs& a, const DevPlan& Pout, const Ptrs8& dst) {
-  using L = Lay<H1, H2>;
+                                          const TcArgs& a, const DevPlan& Pout, const Ptrs8& dst, Sched sc) {
   const int r = q * 32 + lane;
   const uint32_t w3 = smem_u32(smem + L::OFF_W3);
   const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
@@ -185,6 +230,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
   for (int it = 0; it < n_my; ++it) {
     const int b = it & 1;
     mbar_wait(bar + L::B_L2FULL + b, (it >> 1) & 1);
+    if (q == 0 && lane == 0) TR(6, it);
     tc_fence_after();
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -194,7 +240,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
       tmem_wait_ld();
       if (cc == H2 / 32 - 1) {
         tc_fence_before();
-        mbar_arrive(bar + L::B_L2EMPTY + b);
+        arrive_mma<PAIR>(bar + L::B_L2EMPTY + b);
       }
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
@@ -207,8 +253,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
     }
     const float y = act_f(((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + b3,
                           a.act3);
-    const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-    const int64_t row = a.r0 + tile * BM + r;
+    const int64_t row = a.r0 + sc.tile(it) * BM + r;
     bool bad = false;
     if (row < a.r1) {
       bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
@@ -236,15 +281,21 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+    if (q == 0 && lane == 0) TR(7, it);
   }
 }
 
-template <int H1, int H2>
+template <int H1, int H2, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
     mlp3_tc_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
                    const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
                    const __grid_constant__ Ptrs8 dst) {
-  using L = Lay<H1, H2>;
+  constexpr int NS = PAIR ? 2 : 1;
+  using L = Lay<H1, H2, NS>;
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const Sched sc = PAIR ? Sched{(int)blockIdx.x / 2, (int)gridDim.x / 2, (int)rank, 1}
+                        : Sched{(int)blockIdx.x, (int)gridDim.x, 0, 0};
+  const bool leader = rank == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -254,22 +305,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // ---------------------------------------------------------------- setup
   if (threadIdx.x == 0) {
     for (int s = 0; s < XSTAGES; ++s) {
-      mbar_init(bar + L::B_XFULL + s, 128);
+      mbar_init(bar + L::B_XFULL + s, 128 * NS);
       mbar_init(bar + L::B_XEMPTY + s, 1);
     }
     mbar_init(bar + L::B_L1FULL, 1);
-    mbar_init(bar + L::B_L1EMPTY, 256);
+    mbar_init(bar + L::B_L1EMPTY, 256 * NS);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar + L::B_A2FULL + b, 256);
+      mbar_init(bar + L::B_A2FULL + b, 256 * NS);
       mbar_init(bar + L::B_A2EMPTY + b, 1);
       mbar_init(bar + L::B_L2FULL + b, 1);
-      mbar_init(bar + L::B_L2EMPTY + b, 128);
+      mbar_init(bar + L::B_L2EMPTY + b, 128 * NS);
     }
     mbar_fence_init();
   }
-  if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
-  {  // resident weights: blob -> smem (16-byte vectors); ones tile built here
-    const int4* g = reinterpret_cast<const int4*>(a.blob);
+  if (warp == WARP_MMA) {
+    if constexpr (PAIR)
+      tmem_alloc2(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
+  {  // resident weights: this rank's blob -> smem (16-byte vectors); ones tile built here
+    const int4* g = reinterpret_cast<const int4*>(a.blob + rank * L::BLOB);
     for (int i = threadIdx.x; i < L::BLOB_W1 / 16; i += NTHREADS)
       reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
     for (int i = threadIdx.x; i < (L::BLOB_TAIL - L::BLOB_W1) / 16; i += NTHREADS)
@@ -284,10 +340,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   fence_async_smem();
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // peer barriers, weights and TMEM ready before any MMA
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const int n_my = (a.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int n_units = PAIR ? (a.n_tiles + 1) / 2 : a.n_tiles;
+  const int n_my = (n_units - sc.first + sc.stride - 1) / sc.stride;
 
   if (warp >= WARP_LOAD && warp < WARP_MMA) {
     // ============================================================ loader
@@ -297,8 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // tile = 2048 contiguous floats: thread t moves float4 #(t + 128 i), i < 4
       float4 cur[4], nxt[4];
       auto load_tile = [&](int it, float4(&v)[4]) {
-        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-        const int64_t row0 = a.r0 + tile * BM;
+        const int64_t row0 = a.r0 + sc.tile(it) * BM;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int idx = t + 128 * i;
@@ -320,7 +379,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                        pack_bf16(cur[i].z, cur[i].w));
         }
         fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
+        arrive_mma<PAIR>(bar + L::B_XFULL + s);
+        if (t == 0) TR(8, it);
 #pragma unroll
         for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       }
@@ -328,8 +388,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // general plan-driven gather: thread = tile row
       float cur[16], nxt[16];
       auto load_row = [&](int it, float(&v)[16]) {
-        const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
-        const int64_t row = a.r0 + tile * BM + t;
+        const int64_t row = a.r0 + sc.tile(it) * BM + t;
 #pragma unroll
         for (int f = 0; f < 16; ++f) v[f] = 0.0f;
         if (row >= a.r1) return;
@@ -362,16 +421,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
                      pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
         fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
+        arrive_mma<PAIR>(bar + L::B_XFULL + s);
 #pragma unroll
         for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
       }
     }
   } else if (warp == WARP_MMA) {
     // ========================================================= MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc1 = idesc_bf16(BM, H1);
-      constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
+    // (pair: rank 0 issues M = 256 MMAs over both CTAs' SMEM and TMEM)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc1 = idesc_bf16(BM * NS, H1);
+      constexpr uint32_t idesc2 = idesc_bf16(BM * NS, H2);
       const uint32_t w2 = smem_u32(smem + L::OFF_W2);
       const uint32_t x0 = smem_u32(smem + L::OFF_X);
       const uint32_t a20 = smem_u32(smem + L::OFF_A2);
@@ -379,33 +439,55 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint64_t w1bd = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
       const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
       const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
+      auto wait = [&](uint64_t* b, uint32_t ph) {
+        if constexpr (PAIR)
+          mbar_wait_cluster(b, ph);
+        else
+          mbar_wait(b, ph);
+      };
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+        if constexpr (PAIR)
+          mma2_bf16(d, ad, bd, idesc, acc);
+        else
+          mma_bf16(d, ad, bd, idesc, acc);
+      };
+      auto commit = [&](uint64_t* b) {
+        if constexpr (PAIR)
+          mma2_commit_mc(b, 0x3);
+        else
+          mma_commit(b);
+      };
       auto issue_l2 = [&](int j) {
         const int b = j & 1;
-        mbar_wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
-        mbar_wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
+        wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
+        TR(11, j);
+        wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
+        TR(1, j);
         tc_fence_after();
         const uint32_t d = tbase + L::T_L2 + b * H2;
-        mma_bf16(d, onesd, w2bd, idesc2, 0);  // D = b2
+        mma(d, onesd, w2bd, idesc2, 0);  // D = b2
 #pragma unroll
         for (int kc = 0; kc < L::KC; ++kc)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = smem_desc(a20 + b * L::A2_BUF + kc * L::A2_CHUNK + k * 32, 1024, kSwizzle128);
             const uint64_t bd = smem_desc(w2 + kc * L::W2_CHUNK + k * 32, 1024, kSwizzle128);
-            mma_bf16(d, ad, bd, idesc2, 1);
+            mma(d, ad, bd, idesc2, 1);
           }
-        mma_commit(bar + L::B_A2EMPTY + b);
-        mma_commit(bar + L::B_L2FULL + b);
+        commit(bar + L::B_A2EMPTY + b);
+        commit(bar + L::B_L2FULL + b);
       };
       for (int it = 0; it < n_my; ++it) {
         const int s = it % XSTAGES;
-        mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
-        mbar_wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
+        wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
+        TR(9, it);
+        wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
+        TR(0, it);
         tc_fence_after();
-        mma_bf16(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1
-        mma_bf16(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, 1);
-        mma_commit(bar + L::B_XEMPTY + s);
-        mma_commit(bar + L::B_L1FULL);
+        mma(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1
+        mma(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, 1);
+        commit(bar + L::B_XEMPTY + s);
+        commit(bar + L::B_L1FULL);
         if (it > 0) issue_l2(it - 1);
       }
       if (n_my > 0) issue_l2(n_my - 1);
@@ -414,26 +496,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp >= WARP_EPI1) {
     const int half = (warp - WARP_EPI1) >> 2;
     if (a.act1 == SMLRT_RELU)
-      epilogue1<SMLRT_RELU, H1, H2>(smem, bar, tbase, n_my, half, warp & 3, lane);
+      epilogue1<SMLRT_RELU, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane);
     else if (a.act1 == SMLRT_TANH)
-      epilogue1<SMLRT_TANH, H1, H2>(smem, bar, tbase, n_my, half, warp & 3, lane);
+      epilogue1<SMLRT_TANH, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane);
     else
-      epilogue1<SMLRT_IDENTITY, H1, H2>(smem, bar, tbase, n_my, half, warp & 3, lane);
+      epilogue1<SMLRT_IDENTITY, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane);
   } else {
     if (a.act2 == SMLRT_RELU)
-      epilogue2<SMLRT_RELU, H1, H2>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst);
+      epilogue2<SMLRT_RELU, H1, H2, L, PAIR>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
     else if (a.act2 == SMLRT_TANH)
-      epilogue2<SMLRT_TANH, H1, H2>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst);
+      epilogue2<SMLRT_TANH, H1, H2, L, PAIR>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
     else
-      epilogue2<SMLRT_IDENTITY, H1, H2>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst);
+      epilogue2<SMLRT_IDENTITY, H1, H2, L, PAIR>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
   }
 
   // -------------------------------------------------------------- teardown
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == WARP_MMA) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    if constexpr (PAIR)
+      tmem_dealloc2(tbase, 512);
+    else
+      tmem_dealloc(tbase, 512);
   }
 }
 
@@ -506,10 +594,10 @@ uint16_t f2bf(float f) {
   return (uint16_t)(u >> 16);
 }
 
-template <int H1, int H2>
+template <int H1, int H2, int NS>
 std::vector<uint8_t> pack(const smlrt_model_s& m) {
-  using L = Lay<H1, H2>;
-  std::vector<uint8_t> blob(L::BLOB, 0);
+  using L = Lay<H1, H2, NS>;
+  std::vector<uint8_t> blob((size_t)L::BLOB * NS, 0);
   const int F = m.in_features;
   const float* W1 = m.host_params.data();
   const float* b1 = W1 + (size_t)H1 * F;
@@ -517,32 +605,39 @@ std::vector<uint8_t> pack(const smlrt_model_s& m) {
   const float* b2 = W2 + (size_t)H2 * H1;
   const float* W3 = b2 + H2;
   const float* b3 = W3 + H2;
-  auto put = [&](size_t off, float v) {
-    uint16_t h = f2bf(v);
-    std::memcpy(blob.data() + off, &h, 2);
-  };
   auto bf = [](float v) {  // value of the bf16 rounding of v
     uint32_t u = (uint32_t)f2bf(v) << 16;
     float r;
     std::memcpy(&r, &u, 4);
     return r;
   };
-  for (int kc = 0; kc < L::KC; ++kc)
-    for (int n = 0; n < H2; ++n)
-      for (int k = 0; k < 64; ++k) put(kc * L::W2_CHUNK + sw128_offset(n, k), W2[(size_t)n * H1 + kc * 64 + k]);
-  const size_t o_w1 = L::BLOB_W1, o_w1b = o_w1 + H1 * 32, o_w2b = o_w1b + H1 * 32;
-  for (int n = 0; n < H1; ++n) {
-    for (int k = 0; k < KX; ++k) put(o_w1 + sw32_offset(n, k), k < F ? W1[(size_t)n * F + k] : 0.0f);
-    put(o_w1b + sw32_offset(n, 0), b1[n]);
-    put(o_w1b + sw32_offset(n, 1), b1[n] - bf(b1[n]));
+  for (int rk = 0; rk < NS; ++rk) {
+    uint8_t* base = blob.data() + (size_t)rk * L::BLOB;
+    auto put = [&](size_t off, float v) {
+      uint16_t h = f2bf(v);
+      std::memcpy(base + off, &h, 2);
+    };
+    // B operands: this rank's N rows (rk * N/NS ...)
+    for (int kc = 0; kc < L::KC; ++kc)
+      for (int n = 0; n < L::N2; ++n)
+        for (int k = 0; k < 64; ++k)
+          put(kc * L::W2_CHUNK + sw128_offset(n, k), W2[(size_t)(rk * L::N2 + n) * H1 + kc * 64 + k]);
+    const size_t o_w1 = L::BLOB_W1, o_w1b = o_w1 + L::N1 * 32, o_w2b = o_w1b + L::N1 * 32;
+    for (int n = 0; n < L::N1; ++n) {
+      const int gn = rk * L::N1 + n;
+      for (int k = 0; k < KX; ++k) put(o_w1 + sw32_offset(n, k), k < F ? W1[(size_t)gn * F + k] : 0.0f);
+      put(o_w1b + sw32_offset(n, 0), b1[gn]);
+      put(o_w1b + sw32_offset(n, 1), b1[gn] - bf(b1[gn]));
+    }
+    for (int n = 0; n < L::N2; ++n) {
+      const int gn = rk * L::N2 + n;
+      put(o_w2b + sw32_offset(n, 0), b2[gn]);
+      put(o_w2b + sw32_offset(n, 1), b2[gn] - bf(b2[gn]));
+    }
+    float* tail = reinterpret_cast<float*>(base + L::BLOB_TAIL);
+    std::memcpy(tail, W3, H2 * 4);
+    tail[H2] = b3[0];
   }
-  for (int n = 0; n < H2; ++n) {
-    put(o_w2b + sw32_offset(n, 0), b2[n]);
-    put(o_w2b + sw32_offset(n, 1), b2[n] - bf(b2[n]));
-  }
-  float* tail = reinterpret_cast<float*>(blob.data() + L::BLOB_TAIL);
-  std::memcpy(tail, W3, H2 * 4);
-  tail[H2] = b3[0];
   return blob;
 }
 
@@ -560,21 +655,39 @@ int num_sms() {
   return n;
 }
 
+// CTA-pair kernel (SMLRT_TC_PAIR=1); off by default: measured slower than the
+// single-CTA kernel on bonds (period 2800 vs 2390 cycles/tile, tools/tc_trace.py)
+bool use_pair() {
+  static const int v = [] {
+    const char* e = std::getenv("SMLRT_TC_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+template <int H1, int H2>
+constexpr size_t pair_blob_off() {
+  return ((size_t)Lay<H1, H2, 1>::BLOB + 1023) & ~size_t(1023);
+}
+
 template <int H1, int H2>
 int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
            int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
            int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
-  using L = Lay<H1, H2>;
   if (n_in > 8 || n_out > 8) return SMLRT_E_UNSUPPORTED;
+  const bool pair = use_pair();
   static int configured_mask = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured_mask & (1 << dev))) {
-    SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC));
+    SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Lay<H1, H2, 1>::ALLOC));
+    SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Lay<H1, H2, 2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
-  a.blob = reinterpret_cast<const uint8_t*>(m.tc_blob);
+  a.blob = reinterpret_cast<const uint8_t*>(m.tc_blob) + (pair ? pair_blob_off<H1, H2>() : 0);
   a.F = m.in_features;
   a.act1 = m.layers[0].act;
   a.act2 = m.layers[1].act;
@@ -599,8 +712,26 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     const float* base = reinterpret_cast<const float*>(in_ptrs[in.uarray]) + in.col_off0;
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
-  const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-  mlp3_tc_kernel<H1, H2><<<grid, NTHREADS, L::ALLOC, s>>>(a, in, src, out, dst);
+  if (!pair) {
+    const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
+    mlp3_tc_kernel<H1, H2, false><<<grid, NTHREADS, Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
+  } else {
+    const int pairs = (a.n_tiles + 1) / 2;
+    const int grid = 2 * std::max(1, std::min(pairs, num_sms() / 2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = Lay<H1, H2, 2>::ALLOC;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SMLRT_CUDA(cudaLaunchKernelEx(&cfg, mlp3_tc_kernel<H1, H2, true>, a, in, src, out, dst));
+  }
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -674,13 +805,22 @@ __global__ void __launch_bounds__(128, 1) tc_selftest_kernel(const float* A, con
 
 int tc_pack_model(smlrt_model_s& m) {
   if (wide_shape(m)) return wide_pack(m);
-  std::vector<uint8_t> blob;
-  if (shape_is(m, 256, 128))
-    blob = pack<256, 128>(m);
-  else if (shape_is(m, 128, 64))
-    blob = pack<128, 64>(m);
-  else
+  // [single-CTA blob][pad to 1 KB][rank-0 blob][rank-1 blob]
+  std::vector<uint8_t> blob, pair;
+  size_t off = 0;
+  if (shape_is(m, 256, 128)) {
+    blob = pack<256, 128, 1>(m);
+    pair = pack<256, 128, 2>(m);
+    off = pair_blob_off<256, 128>();
+  } else if (shape_is(m, 128, 64)) {
+    blob = pack<128, 64, 1>(m);
+    pair = pack<128, 64, 2>(m);
+    off = pair_blob_off<128, 64>();
+  } else {
     return SMLRT_OK;  // no tcgen05 kernel for this shape; region_infer reports it
+  }
+  blob.resize(off, 0);
+  blob.insert(blob.end(), pair.begin(), pair.end());
   SMLRT_CUDA(cudaMalloc(&m.tc_blob, blob.size()));
   SMLRT_CUDA(cudaMemcpy(m.tc_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice));
   m.tc_bytes = blob.size();
@@ -704,6 +844,12 @@ int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* cons
 }
 
 }  // namespace smlrt
+
+#ifdef SMLRT_TC_TRACE
+extern "C" int smlrt_tc_trace_dump(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, smlrt::g_tc_trace, sizeof(smlrt::g_tc_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int smlrt_tc_selftest(int K, int N, const float* A, const float* B, float* D) {
   using namespace smlrt;

@@ -1,0 +1,48 @@
+"""Pipeline trace of the fused tcgen05 bonds kernel (debug build only).
+
+    make -C paper_2407_18352_b200/csrc trace
+    SMLRT_B200_LIB=paper_2407_18352_b200/libsmlrt_b200_trace.so python tools/tc_trace.py
+
+Prints, for CTA 0, per-tile clock64 deltas of each role's events relative to
+the L1 MMA issue of that tile, and the steady-state period."""
+import ctypes as C
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2407_18352_b200 as sm  # noqa: E402
+from paper_2407_18352_b200 import _native, workloads  # noqa: E402
+
+EV = {0: "L1 issue", 9: "mma sees XFULL", 1: "L2 issue", 11: "mma sees A2FULL", 2: "epi1 L1FULL", 3: "epi1 A2EMPTY",
+      4: "epi1 drained", 5: "epi1 A2FULL", 6: "epi2 L2FULL", 7: "epi2 done", 8: "loader XFULL"}
+
+n = int(os.environ.get("N", 148 * 128 * 64 * 2))
+wl = workloads.make("bonds", n)
+wl.to_device()
+with tempfile.TemporaryDirectory() as d:
+    sm.save_model(wl.model, d + "/m")
+    with sm.Runtime() as rt:
+        h = rt.register_region(wl.descriptor(d + "/m"))
+        rt.invoke_region(h)
+        rt.invoke_region(h)
+import torch  # noqa: E402
+torch.cuda.synchronize()
+lib = _native.lib()
+buf = (C.c_ulonglong * (2 * 64 * 16))()
+assert lib.smlrt_tc_trace_dump(buf) == 0
+t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 64, 16).astype(np.int64)
+for cta in (0, 1):
+    tr = t[cta]
+    base = tr[0, 0] if tr[0, 0] else tr[0, 2]
+    print(f"== CTA {cta} (cycles from tile-0 L1 issue)")
+    print("tile " + " ".join(f"{EV[e][:13]:>13}" for e in (8, 9, 0, 2, 3, 4, 5, 11, 1, 6, 7)))
+    for it in range(0, 24):
+        print(f"{it:4d} " + " ".join(f"{(tr[it, e] - base) if tr[it, e] else -1:13d}" for e in (8, 9, 0, 2, 3, 4, 5, 11, 1, 6, 7)))
+    for e in (0, 1, 2, 5, 7):
+        col = tr[8:60, e]
+        col = col[col > 0]
+        if len(col) > 2:
+            print(f"period({EV[e]}): {np.median(np.diff(col)):.0f} cycles")
