@@ -51,6 +51,8 @@ struct FastDiv {
 // Address of (row r, column c) = col_off[c] + sum_k idx_k(r) * stride(c, k),
 // idx = row-major unravel of r over the sweep shape.  For "uniform" plans all
 // columns share `ustride`, so the row part is computed once per row.
+constexpr int SMLRT_INLINE_COLS = 64;
+
 struct DevPlan {
   int32_t n_sweep;
   int32_t n_cols;
@@ -68,6 +70,7 @@ struct DevPlan {
   int64_t col_off0;         // col_off[0] (host copy, for launch-time decisions)
   int32_t win_w;            // >0: columns form a 2-D window of rows of win_w
   int64_t win_pitch;        //     elements at this pitch (uniform plans)
+  int64_t col_inl[SMLRT_INLINE_COLS];  // col_off copy in the parameter bank (n_cols <= SMLRT_INLINE_COLS)
 };
 
 __host__ __device__ __forceinline__ int64_t row_offset_uniform(const DevPlan& p, uint32_t r) {

@@ -14,7 +14,16 @@
 // tanhf (within 2 ulp, checked at tolerance, as the reference's own tests do).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
+
+#ifndef SMLRT_OPT_R
+#define SMLRT_OPT_R 2
+#endif
+#ifndef SMLRT_OPT_UNR
+#define SMLRT_OPT_UNR 4
+#endif
 
 namespace smlrt {
 namespace {
@@ -49,9 +58,11 @@ __device__ __forceinline__ bool nonfinite(float v) {
   return (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
 }
 
-// np.maximum(y, 0): NaN wins; relu of a finite value is max(y, +0).
+// np.maximum(y, 0): NaN wins, -0 -> +0 (numpy returns +0 for maximum(-0., 0.)).
+__device__ __forceinline__ float relu_exact(float y) { return (y > 0.0f || y != y) ? y : 0.0f; }
+
 __device__ __forceinline__ float activate(float y, int act) {
-  if (act == SMLRT_RELU) return (y < 0.0f) ? 0.0f : y;
+  if (act == SMLRT_RELU) return relu_exact(y);
   if (act == SMLRT_TANH) return tanhf(y);
   return y;
 }
@@ -189,75 +200,169 @@ Ptrs pack(const void* const* ptrs, const int32_t* dts, int n) {
 
 // ========================== fused exact region kernel ==========================
 // The model's parameters travel in the kernel parameter bank (constant bank
-// 0, <= 32 KB since CUDA 12.1), so every multiply reads its weight as a
-// constant operand: 1 FMUL + 1 FADD per multiply-accumulate and no loads.
+// 0, <= 32 KB since CUDA 12.1), packed on the host in the order the unrolled
+// forward pass consumes them and 16-byte aligned, so the compiler fetches
+// four weights per LDCU.128 into uniform registers (one per warp) and every
+// multiply-accumulate is 1 FMUL + 1 FADD with a uniform-register operand.
+// Scalar (unaligned, strided) weight fetches cost one LDCU per multiply and
+// made the kernel MIO-bound (short-scoreboard stalls).
+constexpr int r4(int n) { return (n + 3) & ~3; }
+
 template <int... D>
 struct Shape;
 
+// 1 layer: W [B][r4(A)] row-major (rows padded), b [r4(B)]
 template <int A, int B>
 struct Shape<A, B> {
-  static constexpr int L = 1, IN = A, OUT = B, MAXW = (A > B ? A : B);
-  static constexpr int NPARAM = A * B + B;
+  static constexpr int L = 1, IN = A, OUT = B;
+  static constexpr int SW = r4(A), OB = B * SW;
+  static constexpr int NPARAM = OB + r4(B);
 };
+// 2 layers, streamed: P1[f] = {W1[f][0..A), b1[f]} padded to S1 = r4(A+1);
+// P2[f] = {W2[0..C)[f]} (a column of W2) padded to S2 = r4(C); b2 [r4(C)]
 template <int A, int B, int C>
 struct Shape<A, B, C> {
-  static constexpr int L = 2, IN = A, OUT = C, MAXW = (A > B ? (A > C ? A : C) : (B > C ? B : C));
-  static constexpr int NPARAM = A * B + B + B * C + C;
+  static constexpr int L = 2, IN = A, OUT = C;
+  static constexpr int S1 = r4(A + 1), S2 = r4(C);
+  static constexpr int O2 = B * S1, OB2 = O2 + B * S2;
+  static constexpr int NPARAM = OB2 + r4(C);
 };
+// 3 layers: as above, then W3 [E][r4(C)] row-major, b3 [r4(E)]
 template <int A, int B, int C, int E>
 struct Shape<A, B, C, E> {
   static constexpr int L = 3, IN = A, OUT = E;
-  static constexpr int NPARAM = A * B + B + B * C + C + C * E + E;
+  static constexpr int S1 = r4(A + 1), S2 = r4(C), S3 = r4(C);
+  static constexpr int O2 = B * S1, OB2 = O2 + B * S2, O3 = OB2 + r4(C), OB3 = O3 + E * S3;
+  static constexpr int NPARAM = OB3 + r4(E);
 };
 
 template <int NP, int NL>
-struct ModelParams {
-  int act[NL];
+struct alignas(16) ModelParams {
   float w[NP];
+  int act[NL];
 };
 
-template <int IN, int OUT>
+// y[j] = act(ordered dot(x, W[j, :]) + b[j]); W rows at stride SW
+template <int IN, int OUT, int SW>
 __device__ __forceinline__ void layer_exact(const float (&x)[IN], float (&y)[OUT], const float* W,
                                             const float* b, int act) {
 #pragma unroll
   for (int j = 0; j < OUT; ++j) {
     float acc = 0.0f;
 #pragma unroll
-    for (int f = 0; f < IN; ++f) acc = __fadd_rn(acc, __fmul_rn(x[f], W[j * IN + f]));
+    for (int f = 0; f < IN; ++f) acc = __fadd_rn(acc, __fmul_rn(x[f], W[j * SW + f]));
     y[j] = __fadd_rn(acc, b[j]);
   }
   // activation under one warp-uniform branch, so the matvec above exists once
   if (act == SMLRT_RELU) {
 #pragma unroll
-    for (int j = 0; j < OUT; ++j) y[j] = (y[j] < 0.0f) ? 0.0f : y[j];
+    for (int j = 0; j < OUT; ++j) y[j] = relu_exact(y[j]);
   } else if (act == SMLRT_TANH) {
 #pragma unroll
     for (int j = 0; j < OUT; ++j) y[j] = tanhf(y[j]);
   }
 }
 
-template <int A, int B>
+template <int ACT>
+__device__ __forceinline__ float act_c(float y) {
+  if constexpr (ACT == SMLRT_RELU) return relu_exact(y);
+  else if constexpr (ACT == SMLRT_TANH) return tanhf(y);
+  else return y;
+}
+
+// Layers 1 and 2 streamed: hidden unit f of layer 1 is finished (ordered dot,
+// + b1[f], act1) and immediately folded into every layer-2 accumulator,
+// acc[j] = acc[j] + h_f * W2[j, f] in ascending f -- the same operation
+// sequence per output as _matmul_rowwise (models.py:188-194), so bitwise equal,
+// but only the C accumulators (not all B hidden values) are live: ~4x fewer
+// registers than materialising h1, hence 4x the resident warps.
+template <int ACT1, int A, int B, int C, int S1, int S2, int R, int UNR>
+__device__ __forceinline__ void layers12_streamed(const float* P1, const float* P2, const float* b2, int act2,
+                                                  const float (&x)[R][A], float (&y)[R][C]) {
+  float acc[R][C];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) acc[r][j] = 0.0f;
+  // partial unroll keeps the loop body inside the instruction cache (a fully
+  // unrolled 5-64-32 body stalls on instruction fetch); f stays warp-uniform,
+  // so the weights are still fetched as uniform LDCU.128s
+#pragma unroll UNR
+  for (int f = 0; f < B; ++f) {
+    float h[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      h[r] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < A; ++i) h[r] = __fadd_rn(h[r], __fmul_rn(x[r][i], P1[f * S1 + i]));
+      h[r] = act_c<ACT1>(__fadd_rn(h[r], P1[f * S1 + A]));
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r][j] = __fadd_rn(acc[r][j], __fmul_rn(h[r], P2[f * S2 + j]));
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) y[r][j] = activate(__fadd_rn(acc[r][j], b2[j]), act2);
+}
+
+template <int ACT1, int R, int UNR, int A, int B>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B>::NPARAM, 1>& mp,
-                                        const float (&x)[A], float (&y)[B]) {
-  layer_exact<A, B>(x, y, mp.w, mp.w + A * B, mp.act[0]);
+                                        const float (&x)[R][A], float (&y)[R][B]) {
+  using S = Shape<A, B>;
+#pragma unroll
+  for (int r = 0; r < R; ++r) layer_exact<A, B, S::SW>(x[r], y[r], mp.w, mp.w + S::OB, mp.act[0]);
+}
+template <int ACT1, int R, int UNR, int A, int B, int C>
+__device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C>::NPARAM, 2>& mp,
+                                        const float (&x)[R][A], float (&y)[R][C]) {
+  using S = Shape<A, B, C>;
+  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, R, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], x, y);
+}
+template <int ACT1, int R, int UNR, int A, int B, int C, int E>
+__device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C, E>::NPARAM, 3>& mp,
+                                        const float (&x)[R][A], float (&y)[R][E]) {
+  using S = Shape<A, B, C, E>;
+  float h2[R][C];
+  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, R, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], x, h2);
+#pragma unroll
+  for (int r = 0; r < R; ++r) layer_exact<C, E, S::S3>(h2[r], y[r], mp.w + S::O3, mp.w + S::OB3, mp.act[2]);
+}
+
+// host: model.host_params ([W (out x in), b] per layer, row-major) -> the
+// packed use-order layout above
+template <int A, int B>
+void pack_params(const float* hp, float* w, Shape<A, B>*) {
+  using S = Shape<A, B>;
+  for (int j = 0; j < B; ++j)
+    for (int f = 0; f < A; ++f) w[j * S::SW + f] = hp[j * A + f];
+  for (int j = 0; j < B; ++j) w[S::OB + j] = hp[A * B + j];
 }
 template <int A, int B, int C>
-__device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C>::NPARAM, 2>& mp,
-                                        const float (&x)[A], float (&y)[C]) {
-  float h[B];
-  layer_exact<A, B>(x, h, mp.w, mp.w + A * B, mp.act[0]);
-  constexpr int o = A * B + B;
-  layer_exact<B, C>(h, y, mp.w + o, mp.w + o + B * C, mp.act[1]);
+void pack12(const float* hp, float* w, int S1, int S2, int O2, int OB2) {
+  const float *W1 = hp, *b1 = W1 + A * B, *W2 = b1 + B, *b2 = W2 + B * C;
+  for (int f = 0; f < B; ++f) {
+    for (int i = 0; i < A; ++i) w[f * S1 + i] = W1[f * A + i];
+    w[f * S1 + A] = b1[f];
+    for (int j = 0; j < C; ++j) w[O2 + f * S2 + j] = W2[j * B + f];
+  }
+  for (int j = 0; j < C; ++j) w[OB2 + j] = b2[j];
+}
+template <int A, int B, int C>
+void pack_params(const float* hp, float* w, Shape<A, B, C>*) {
+  using S = Shape<A, B, C>;
+  pack12<A, B, C>(hp, w, S::S1, S::S2, S::O2, S::OB2);
 }
 template <int A, int B, int C, int E>
-__device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C, E>::NPARAM, 3>& mp,
-                                        const float (&x)[A], float (&y)[E]) {
-  float h1[B], h2[C];
-  layer_exact<A, B>(x, h1, mp.w, mp.w + A * B, mp.act[0]);
-  constexpr int o1 = A * B + B;
-  layer_exact<B, C>(h1, h2, mp.w + o1, mp.w + o1 + B * C, mp.act[1]);
-  constexpr int o2 = o1 + B * C + C;
-  layer_exact<C, E>(h2, y, mp.w + o2, mp.w + o2 + C * E, mp.act[2]);
+void pack_params(const float* hp, float* w, Shape<A, B, C, E>*) {
+  using S = Shape<A, B, C, E>;
+  pack12<A, B, C>(hp, w, S::S1, S::S2, S::O2, S::OB2);
+  const float *W3 = hp + A * B + B + B * C + C, *b3 = W3 + C * E;
+  for (int j = 0; j < E; ++j)
+    for (int f = 0; f < C; ++f) w[S::O3 + j * S::S3 + f] = W3[j * C + f];
+  for (int j = 0; j < E; ++j) w[S::OB3 + j] = b3[j];
 }
 
 template <bool F32, int IN>
@@ -268,7 +373,7 @@ __device__ __forceinline__ void load_row(const DevPlan& P, const Ptrs& src, uint
     int dt = src.dt[P.uarray];
 #pragma unroll
     for (int f = 0; f < IN; ++f) {
-      int64_t a = __ldg(P.col_off + f) + ro;
+      int64_t a = (IN <= SMLRT_INLINE_COLS ? P.col_inl[f] : __ldg(P.col_off + f)) + ro;
       x[f] = F32 ? __ldg(reinterpret_cast<const float*>(base) + a) : load_as_f32(base, dt, a);
     }
   } else {
@@ -282,33 +387,46 @@ __device__ __forceinline__ void load_row(const DevPlan& P, const Ptrs& src, uint
   }
 }
 
-template <bool F32, class S, int... D>
+// R rows per thread (rows blockIdx*128*R + threadIdx + 128 r: coalesced per r)
+template <bool F32, int ACT1, int R, int UNR, class S, int... D>
 __global__ void __launch_bounds__(128) region_exact_kernel(
     const ModelParams<S::NPARAM, S::L> mp, const __grid_constant__ DevPlan Pin,
     const __grid_constant__ Ptrs src, const __grid_constant__ DevPlan Pout,
     const __grid_constant__ Ptrs dst, int64_t r0, int64_t r1, float* __restrict__ staged, uint32_t* status) {
-  int64_t row = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t row0 = r0 + blockIdx.x * (int64_t)(128 * R) + threadIdx.x;
   bool bad = false;
-  if (row < r1) {
-    float x[S::IN], y[S::OUT];
-    load_row<F32>(Pin, src, (uint32_t)row, x);
-    forward<D...>(mp, x, y);
+  float x[R][S::IN], y[R][S::OUT];
 #pragma unroll
-    for (int g = 0; g < S::OUT; ++g) bad |= nonfinite(y[g]);
+  for (int r = 0; r < R; ++r) {
+    const int64_t row = row0 + 128 * r;
+    if (row < r1) {
+      load_row<F32>(Pin, src, (uint32_t)row, x[r]);
+    } else {
+#pragma unroll
+      for (int f = 0; f < S::IN; ++f) x[r][f] = 0.0f;
+    }
+  }
+  forward<ACT1, R, UNR, D...>(mp, x, y);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t row = row0 + 128 * r;
+    if (row >= r1) continue;
+#pragma unroll
+    for (int g = 0; g < S::OUT; ++g) bad |= nonfinite(y[r][g]);
     if (staged != nullptr) {
 #pragma unroll
-      for (int g = 0; g < S::OUT; ++g) staged[(row - r0) * S::OUT + g] = y[g];
+      for (int g = 0; g < S::OUT; ++g) staged[(row - r0) * S::OUT + g] = y[r][g];
     } else if (Pout.uniform) {
       int64_t ro = row_offset_uniform(Pout, (uint32_t)row);
       void* base = const_cast<void*>(dst.p[Pout.uarray]);
       int dt = dst.dt[Pout.uarray];
 #pragma unroll
       for (int g = 0; g < S::OUT; ++g) {
-        int64_t a = __ldg(Pout.col_off + g) + ro;
+        int64_t a = (S::OUT <= SMLRT_INLINE_COLS ? Pout.col_inl[g] : __ldg(Pout.col_off + g)) + ro;
         if (F32)
-          reinterpret_cast<float*>(base)[a] = y[g];
+          reinterpret_cast<float*>(base)[a] = y[r][g];
         else
-          store_f32(base, dt, a, y[g]);
+          store_f32(base, dt, a, y[r][g]);
       }
     } else {
       uint32_t idx[SMLRT_MAX_SWEEP];
@@ -316,7 +434,7 @@ __global__ void __launch_bounds__(128) region_exact_kernel(
 #pragma unroll
       for (int g = 0; g < S::OUT; ++g) {
         int arr = __ldg(Pout.col_arr + g);
-        store_f32(const_cast<void*>(dst.p[arr]), dst.dt[arr], col_address(Pout, g, idx), y[g]);
+        store_f32(const_cast<void*>(dst.p[arr]), dst.dt[arr], col_address(Pout, g, idx), y[r][g]);
       }
     }
   }
@@ -333,6 +451,16 @@ bool dims_match(const smlrt_model_s& m) {
   return true;
 }
 
+// rows per thread / layer-1 loop unroll per shape (measured on B200)
+template <int... D>
+struct Tune {
+  static constexpr int R = 1, UNR = 64;
+};
+template <>
+struct Tune<5, 64, 32, 1> {
+  static constexpr int R = SMLRT_OPT_R, UNR = SMLRT_OPT_UNR;
+};
+
 template <int... D>
 int try_fused(const smlrt_model_s& m, const DevPlan& in, const Ptrs& src, const DevPlan& out,
               const Ptrs& dst, bool all_f32, int64_t r0, int64_t r1, float* staged, cudaStream_t s,
@@ -341,15 +469,28 @@ int try_fused(const smlrt_model_s& m, const DevPlan& in, const Ptrs& src, const 
   if (*done || !dims_match<D...>(m)) return SMLRT_OK;
   *done = true;
   if (probe_only) return SMLRT_OK;
-  ModelParams<S::NPARAM, S::L> mp;
+  ModelParams<S::NPARAM, S::L> mp{};
   for (int l = 0; l < S::L; ++l) mp.act[l] = m.layers[l].act;
-  for (int i = 0; i < S::NPARAM; ++i) mp.w[i] = m.host_params[i];
+  pack_params(m.host_params.data(), mp.w, static_cast<S*>(nullptr));
   int64_t n = r1 - r0;
-  dim3 grid((unsigned)((n + 127) / 128));
-  if (all_f32)
-    region_exact_kernel<true, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged, status);
+  constexpr int R = Tune<D...>::R, UNR = Tune<D...>::UNR;
+  dim3 grid((unsigned)((n + 128 * R - 1) / (128 * R)));
+  // layer-1 activation is a template argument (it sits inside the streamed loop)
+  auto go = [&](auto act1) {
+    constexpr int A1 = decltype(act1)::value;
+    if (all_f32)
+      region_exact_kernel<true, A1, R, UNR, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged,
+                                                                          status);
+    else
+      region_exact_kernel<false, A1, R, UNR, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged,
+                                                                           status);
+  };
+  if (S::L == 1 || m.layers[0].act == SMLRT_IDENTITY)
+    go(std::integral_constant<int, SMLRT_IDENTITY>{});
+  else if (m.layers[0].act == SMLRT_RELU)
+    go(std::integral_constant<int, SMLRT_RELU>{});
   else
-    region_exact_kernel<false, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged, status);
+    go(std::integral_constant<int, SMLRT_TANH>{});
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }

@@ -93,6 +93,7 @@ int smlrt_plan_s::tables(DevPlan* p) {
   p->col_off0 = col_off.empty() ? 0 : col_off[0];
   p->win_w = win_w;
   p->win_pitch = win_pitch;
+  for (int c = 0; c < n_cols && c < SMLRT_INLINE_COLS; ++c) p->col_inl[c] = col_off[c];
   p->col_off = it->second.col_off;
   p->col_arr = it->second.col_arr;
   p->col_str = it->second.col_str;
