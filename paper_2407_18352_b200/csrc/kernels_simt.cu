@@ -14,15 +14,13 @@
 // tanhf (within 2 ulp, checked at tolerance, as the reference's own tests do).
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
 
-#ifndef SMLRT_OPT_R
-#define SMLRT_OPT_R 2
-#endif
 #ifndef SMLRT_OPT_UNR
-#define SMLRT_OPT_UNR 4
+#define SMLRT_OPT_UNR 8
 #endif
 
 namespace smlrt {
@@ -218,12 +216,14 @@ struct Shape<A, B> {
   static constexpr int SW = r4(A), OB = B * SW;
   static constexpr int NPARAM = OB + r4(B);
 };
-// 2 layers, streamed: P1[f] = {W1[f][0..A), b1[f]} padded to S1 = r4(A+1);
-// P2[f] = {W2[0..C)[f]} (a column of W2) padded to S2 = r4(C); b2 [r4(C)]
+// 2 layers, streamed over a row pair: P1[f] = {W1[f][0..A), b1[f]}, each value
+// duplicated (w, w) for the row-paired f32x2 ops, padded to S1 = r4(2(A+1));
+// P2[f] = {W2[0..C)[f]} (a column of W2, output-paired) padded to S2 = r4(C);
+// b2 [r4(C)]
 template <int A, int B, int C>
 struct Shape<A, B, C> {
   static constexpr int L = 2, IN = A, OUT = C;
-  static constexpr int S1 = r4(A + 1), S2 = r4(C);
+  static constexpr int S1 = r4(2 * (A + 1)), S2 = r4(C);
   static constexpr int O2 = B * S1, OB2 = O2 + B * S2;
   static constexpr int NPARAM = OB2 + r4(C);
 };
@@ -231,7 +231,7 @@ struct Shape<A, B, C> {
 template <int A, int B, int C, int E>
 struct Shape<A, B, C, E> {
   static constexpr int L = 3, IN = A, OUT = E;
-  static constexpr int S1 = r4(A + 1), S2 = r4(C), S3 = r4(C);
+  static constexpr int S1 = r4(2 * (A + 1)), S2 = r4(C), S3 = r4(C);
   static constexpr int O2 = B * S1, OB2 = O2 + B * S2, O3 = OB2 + r4(C), OB3 = O3 + E * S3;
   static constexpr int NPARAM = OB3 + r4(E);
 };
@@ -239,8 +239,36 @@ struct Shape<A, B, C, E> {
 template <int NP, int NL>
 struct alignas(16) ModelParams {
   float w[NP];
+  uint64_t one2;  // (1.0f, 1.0f): opaque to ptxas, see add2()
   int act[NL];
 };
+
+// ---- packed f32x2 arithmetic (sm_100 FMUL2 / FFMA2), bitwise IEEE RN ----
+// ptxas contracts mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2 (even with
+// --fmad=false), which would change the rounding.  The add is therefore
+// written as fma(p, one, acc) with `one` = (1, 1) read from the parameter
+// bank: RN(p*1 + acc) == RN(p + acc) exactly (also for signed zeros, NaN and
+// infinities), and ptxas cannot fold a multiply into it.
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t acc, uint64_t p, uint64_t one) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(p), "l"(one), "l"(acc));
+  return r;
+}
+__device__ __forceinline__ uint64_t ldw2(const float* w) { return *reinterpret_cast<const uint64_t*>(w); }
+__device__ __forceinline__ ulonglong2 ldw4(const float* w) { return *reinterpret_cast<const ulonglong2*>(w); }
 
 // y[j] = act(ordered dot(x, W[j, :]) + b[j]); W rows at stride SW
 template <int IN, int OUT, int SW>
@@ -276,36 +304,63 @@ __device__ __forceinline__ float act_c(float y) {
 // sequence per output as _matmul_rowwise (models.py:188-194), so bitwise equal,
 // but only the C accumulators (not all B hidden values) are live: ~4x fewer
 // registers than materialising h1, hence 4x the resident warps.
-template <int ACT1, int A, int B, int C, int S1, int S2, int R, int UNR>
+//
+// Two rows (a, b) per thread share every instruction: layer 1 runs on row
+// pairs (x_a[i], x_b[i]) x (w, w) with duplicated weights; layer 2 on output
+// pairs (h, h) x (W2[j, f], W2[j+1, f]).  Each FMUL2/FFMA2 does the work of
+// two FMUL/FADD, halving the issue slots of the (issue-bound) kernel.
+template <int ACT1, int A, int B, int C, int S1, int S2, int UNR>
 __device__ __forceinline__ void layers12_streamed(const float* P1, const float* P2, const float* b2, int act2,
-                                                  const float (&x)[R][A], float (&y)[R][C]) {
-  float acc[R][C];
+                                                  uint64_t one, const float (&x)[2][A], float (&y)[2][C]) {
+  static_assert(C % 2 == 0, "output-paired layer 2 needs an even width");
+  uint64_t xp[A];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int i = 0; i < A; ++i) xp[i] = pk2(x[0][i], x[1][i]);
+  uint64_t acc[2][C / 2];
 #pragma unroll
-    for (int j = 0; j < C; ++j) acc[r][j] = 0.0f;
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int j = 0; j < C / 2; ++j) acc[r][j] = 0ull;
   // partial unroll keeps the loop body inside the instruction cache (a fully
   // unrolled 5-64-32 body stalls on instruction fetch); f stays warp-uniform,
   // so the weights are still fetched as uniform LDCU.128s
 #pragma unroll UNR
   for (int f = 0; f < B; ++f) {
-    float h[R];
+    // explicit 16-byte weight fetches: the compiler cannot prove the alignment
+    // of P1 + f * S1 under the partial unroll and would issue 8-byte LDCUs
+    uint64_t w1[S1 / 2];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      h[r] = 0.0f;
-#pragma unroll
-      for (int i = 0; i < A; ++i) h[r] = __fadd_rn(h[r], __fmul_rn(x[r][i], P1[f * S1 + i]));
-      h[r] = act_c<ACT1>(__fadd_rn(h[r], P1[f * S1 + A]));
+    for (int i = 0; i < S1 / 4; ++i) {
+      const ulonglong2 q = ldw4(P1 + f * S1 + 4 * i);
+      w1[2 * i] = q.x;
+      w1[2 * i + 1] = q.y;
     }
+    uint64_t h = 0ull;
 #pragma unroll
-    for (int j = 0; j < C; ++j)
+    for (int i = 0; i < A; ++i) h = add2(h, mul2(xp[i], w1[i]), one);
+    h = add2(h, w1[A], one);  // + b1[f]
+    float ha, hb;
+    upk2(h, ha, hb);
+    ha = act_c<ACT1>(ha);
+    hb = act_c<ACT1>(hb);
+    const uint64_t hha = pk2(ha, ha), hhb = pk2(hb, hb);
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r][j] = __fadd_rn(acc[r][j], __fmul_rn(h[r], P2[f * S2 + j]));
+    for (int j = 0; j < C / 2; ++j) {
+      const ulonglong2 q = ldw4(P2 + f * S2 + 4 * (j / 2));
+      const uint64_t w = (j & 1) ? q.y : q.x;
+      acc[0][j] = add2(acc[0][j], mul2(hha, w), one);
+      acc[1][j] = add2(acc[1][j], mul2(hhb, w), one);
+    }
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int j = 0; j < C; ++j) y[r][j] = activate(__fadd_rn(acc[r][j], b2[j]), act2);
+    for (int j = 0; j < C / 2; ++j) {
+      float lo, hi;
+      upk2(add2(acc[r][j], ldw2(b2 + 2 * j), one), lo, hi);  // acc + b2
+      y[r][2 * j] = activate(lo, act2);
+      y[r][2 * j + 1] = activate(hi, act2);
+    }
 }
 
 template <int ACT1, int R, int UNR, int A, int B>
@@ -319,14 +374,17 @@ template <int ACT1, int R, int UNR, int A, int B, int C>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C>::NPARAM, 2>& mp,
                                         const float (&x)[R][A], float (&y)[R][C]) {
   using S = Shape<A, B, C>;
-  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, R, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], x, y);
+  static_assert(R == 2, "2/3-layer shapes run on row pairs");
+  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x, y);
 }
 template <int ACT1, int R, int UNR, int A, int B, int C, int E>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C, E>::NPARAM, 3>& mp,
                                         const float (&x)[R][A], float (&y)[R][E]) {
   using S = Shape<A, B, C, E>;
+  static_assert(R == 2, "2/3-layer shapes run on row pairs");
   float h2[R][C];
-  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, R, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], x, h2);
+  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x,
+                                                      h2);
 #pragma unroll
   for (int r = 0; r < R; ++r) layer_exact<C, E, S::S3>(h2[r], y[r], mp.w + S::O3, mp.w + S::OB3, mp.act[2]);
 }
@@ -344,8 +402,8 @@ template <int A, int B, int C>
 void pack12(const float* hp, float* w, int S1, int S2, int O2, int OB2) {
   const float *W1 = hp, *b1 = W1 + A * B, *W2 = b1 + B, *b2 = W2 + B * C;
   for (int f = 0; f < B; ++f) {
-    for (int i = 0; i < A; ++i) w[f * S1 + i] = W1[f * A + i];
-    w[f * S1 + A] = b1[f];
+    for (int i = 0; i < A; ++i) w[f * S1 + 2 * i] = w[f * S1 + 2 * i + 1] = W1[f * A + i];
+    w[f * S1 + 2 * A] = w[f * S1 + 2 * A + 1] = b1[f];
     for (int j = 0; j < C; ++j) w[O2 + f * S2 + j] = W2[j * B + f];
   }
   for (int j = 0; j < C; ++j) w[OB2 + j] = b2[j];
@@ -456,9 +514,17 @@ template <int... D>
 struct Tune {
   static constexpr int R = 1, UNR = 64;
 };
+template <int A, int B, int C>
+struct Tune<A, B, C> {
+  static constexpr int R = 2, UNR = B;
+};
+template <int A, int B, int C, int E>
+struct Tune<A, B, C, E> {
+  static constexpr int R = 2, UNR = B;
+};
 template <>
 struct Tune<5, 64, 32, 1> {
-  static constexpr int R = SMLRT_OPT_R, UNR = SMLRT_OPT_UNR;
+  static constexpr int R = 2, UNR = SMLRT_OPT_UNR;
 };
 
 template <int... D>
@@ -472,6 +538,8 @@ int try_fused(const smlrt_model_s& m, const DevPlan& in, const Ptrs& src, const 
   ModelParams<S::NPARAM, S::L> mp{};
   for (int l = 0; l < S::L; ++l) mp.act[l] = m.layers[l].act;
   pack_params(m.host_params.data(), mp.w, static_cast<S*>(nullptr));
+  const float one[2] = {1.0f, 1.0f};
+  std::memcpy(&mp.one2, one, sizeof(one));
   int64_t n = r1 - r0;
   constexpr int R = Tune<D...>::R, UNR = Tune<D...>::UNR;
   dim3 grid((unsigned)((n + 128 * R - 1) / (128 * R)));
