@@ -423,11 +423,25 @@ void pack_params(const float* hp, float* w, Shape<A, B, C, E>*) {
   for (int j = 0; j < E; ++j) w[S::OB3 + j] = b3[j];
 }
 
-template <bool F32, int IN>
+// RUN > 1 (f32 uniform plans whose columns come in contiguous runs of RUN
+// elements, checked at launch): one 64-bit address per run, the run's
+// elements at immediate offsets -- the halo gather's address arithmetic
+// otherwise outweighs its loads.
+template <bool F32, int RUN, int IN>
 __device__ __forceinline__ void load_row(const DevPlan& P, const Ptrs& src, uint32_t r, float (&x)[IN]) {
   if (P.uniform) {
     int64_t ro = row_offset_uniform(P, r);
     const void* base = src.p[P.uarray];
+    if constexpr (F32 && RUN > 1 && IN <= SMLRT_INLINE_COLS && IN % RUN == 0) {
+      const float* pr = reinterpret_cast<const float*>(base) + ro;
+#pragma unroll
+      for (int g = 0; g < IN / RUN; ++g) {
+        const float* q = pr + P.col_inl[g * RUN];
+#pragma unroll
+        for (int k = 0; k < RUN; ++k) x[g * RUN + k] = __ldg(q + k);
+      }
+      return;
+    }
     int dt = src.dt[P.uarray];
 #pragma unroll
     for (int f = 0; f < IN; ++f) {
@@ -445,8 +459,16 @@ __device__ __forceinline__ void load_row(const DevPlan& P, const Ptrs& src, uint
   }
 }
 
+// columns of a uniform plan form contiguous runs of `run` elements
+inline bool plan_runs(const DevPlan& P, int run) {
+  if (!P.uniform || P.n_cols > SMLRT_INLINE_COLS || P.n_cols % run != 0) return false;
+  for (int c = 0; c < P.n_cols; ++c)
+    if (P.col_inl[c] != P.col_inl[c - c % run] + c % run) return false;
+  return true;
+}
+
 // R rows per thread (rows blockIdx*128*R + threadIdx + 128 r: coalesced per r)
-template <bool F32, int ACT1, int R, int UNR, class S, int... D>
+template <bool F32, int ACT1, int R, int UNR, int RUN, class S, int... D>
 __global__ void __launch_bounds__(128) region_exact_kernel(
     const ModelParams<S::NPARAM, S::L> mp, const __grid_constant__ DevPlan Pin,
     const __grid_constant__ Ptrs src, const __grid_constant__ DevPlan Pout,
@@ -458,7 +480,7 @@ __global__ void __launch_bounds__(128) region_exact_kernel(
   for (int r = 0; r < R; ++r) {
     const int64_t row = row0 + 128 * r;
     if (row < r1) {
-      load_row<F32>(Pin, src, (uint32_t)row, x[r]);
+      load_row<F32, RUN>(Pin, src, (uint32_t)row, x[r]);
     } else {
 #pragma unroll
       for (int f = 0; f < S::IN; ++f) x[r][f] = 0.0f;
@@ -478,13 +500,14 @@ __global__ void __launch_bounds__(128) region_exact_kernel(
       int64_t ro = row_offset_uniform(Pout, (uint32_t)row);
       void* base = const_cast<void*>(dst.p[Pout.uarray]);
       int dt = dst.dt[Pout.uarray];
+      float* pr = reinterpret_cast<float*>(base) + ro;  // one row address, column offsets added
 #pragma unroll
       for (int g = 0; g < S::OUT; ++g) {
-        int64_t a = (S::OUT <= SMLRT_INLINE_COLS ? Pout.col_inl[g] : __ldg(Pout.col_off + g)) + ro;
+        const int64_t c = S::OUT <= SMLRT_INLINE_COLS ? Pout.col_inl[g] : __ldg(Pout.col_off + g);
         if (F32)
-          reinterpret_cast<float*>(base)[a] = y[r][g];
+          pr[c] = y[r][g];
         else
-          store_f32(base, dt, a, y[r][g]);
+          store_f32(base, dt, c + ro, y[r][g]);
       }
     } else {
       uint32_t idx[SMLRT_MAX_SWEEP];
@@ -510,21 +533,26 @@ bool dims_match(const smlrt_model_s& m) {
 }
 
 // rows per thread / layer-1 loop unroll per shape (measured on B200)
+// RUN: contiguous input-column run the gather exploits when the plan has it
 template <int... D>
 struct Tune {
-  static constexpr int R = 1, UNR = 64;
+  static constexpr int R = 1, UNR = 64, RUN = 1;
 };
 template <int A, int B, int C>
 struct Tune<A, B, C> {
-  static constexpr int R = 2, UNR = B;
+  static constexpr int R = 2, UNR = B, RUN = 1;
 };
 template <int A, int B, int C, int E>
 struct Tune<A, B, C, E> {
-  static constexpr int R = 2, UNR = B;
+  static constexpr int R = 2, UNR = B, RUN = 1;
 };
 template <>
-struct Tune<5, 64, 32, 1> {
-  static constexpr int R = 2, UNR = SMLRT_OPT_UNR;
+struct Tune<5, 64, 32, 1> {  // C1: [k, 0:5] rows
+  static constexpr int R = 2, UNR = SMLRT_OPT_UNR, RUN = 5;
+};
+template <>
+struct Tune<36, 8, 4> {  // C5: 3x3x4 halo = 12 runs of 3
+  static constexpr int R = 2, UNR = 8, RUN = 3;
 };
 
 template <int... D>
@@ -544,14 +572,19 @@ int try_fused(const smlrt_model_s& m, const DevPlan& in, const Ptrs& src, const 
   constexpr int R = Tune<D...>::R, UNR = Tune<D...>::UNR;
   dim3 grid((unsigned)((n + 128 * R - 1) / (128 * R)));
   // layer-1 activation is a template argument (it sits inside the streamed loop)
+  constexpr int RUN = Tune<D...>::RUN;
+  const bool runs = RUN > 1 && plan_runs(in, RUN);
   auto go = [&](auto act1) {
     constexpr int A1 = decltype(act1)::value;
-    if (all_f32)
-      region_exact_kernel<true, A1, R, UNR, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged,
-                                                                          status);
+    if (all_f32 && runs)
+      region_exact_kernel<true, A1, R, UNR, RUN, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1,
+                                                                               staged, status);
+    else if (all_f32)
+      region_exact_kernel<true, A1, R, UNR, 1, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged,
+                                                                             status);
     else
-      region_exact_kernel<false, A1, R, UNR, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1, staged,
-                                                                           status);
+      region_exact_kernel<false, A1, R, UNR, 1, S, D...><<<grid, 128, 0, s>>>(mp, in, src, out, dst, r0, r1,
+                                                                              staged, status);
   };
   if (S::L == 1 || m.layers[0].act == SMLRT_IDENTITY)
     go(std::integral_constant<int, SMLRT_IDENTITY>{});
