@@ -16,7 +16,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -280,6 +282,309 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   }
 }
 
+// ------------------------------------------------ fused layers 1 + 2 (C3)
+// D2[128 x NH*256] = act1(X W1^T + b1) W2^T for a 128-row tile, the layer-1
+// activations never leaving the SM: four producer warps gather the tile's rows
+// through the in-plan and compute layer 1 on the CUDA cores (packed FFMA2,
+// bf16-valued x and W1, fp32 sums) one 64-wide K chunk at a time, writing it
+// in the SW128 K-major A layout straight into the A ring; the MMA thread
+// consumes it against TMA-streamed W2 chunks.  Replaces the materialised
+// [rows x H1] layer-1 output, which made layer 1 an HBM-write-bound kernel.
+//
+// warp 0: TMA (W2 [256 x 64] boxes)     warp 1: MMA issuer
+// warps 2..: epilogue, 4 per 256-column half (thread = row)
+// last 8 warps: layer-1 producer (thread = row; warps 0-3 / 4-7 of them take
+//   the low / high 32 columns of each 64-wide chunk)
+// warp 0 TMA, warp 1 MMA, warps 2 .. 2+4NH-1 epilogue (4 per N-half), then 4 producer warps
+constexpr int L12_PW = 8;  // producer warps: 2 per SM sub-partition (latency hiding)
+template <int NH>
+constexpr int l12_threads() { return 32 * (2 + 4 * NH + L12_PW); }
+constexpr int L12_SA = 3, L12_SB = 4;
+constexpr int L12_H1MAX = 1024;
+
+template <int NH>
+struct L12Lay {
+  static constexpr int A_BYTES = GBM * 64 * 2;
+  static constexpr int B_BYTES = 256 * 64 * 2;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + L12_SA * A_BYTES;
+  static constexpr int OFF_W1 = OFF_B + L12_SB * B_BYTES;  // per k pair: 8 float2 (7 weight slots, bias)
+  static constexpr int OFF_B2 = OFF_W1 + L12_H1MAX / 2 * 64;
+  static constexpr int OFF_BAR = OFF_B2 + NH * 256 * 4;
+  enum { AFULL = 0, AEMPTY = L12_SA, BFULL = 2 * L12_SA, BEMPTY = BFULL + L12_SB, TFULL = BEMPTY + L12_SB,
+         TEMPTY = TFULL + 1, NBAR = TEMPTY + NH };
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
+  static_assert(ALLOC <= 232448, "shared memory budget");
+};
+
+struct L12Args {
+  int M, H1, F;
+  int act1, act2;
+  int64_t r0;               // sweep row of tile row 0
+  const float* w1p;         // [H1/2][16] f32: slot f < 7 = (W1[2p][f], W1[2p+1][f]) (bf16-valued), slot 7 = (b1[2p], b1[2p+1])
+  const float* b2;          // [NH*256]
+  const void* src;          // in-plan's array
+  int src_dt;
+  __nv_bfloat16* out;       // [M][NH*256]
+};
+
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2pk(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
+template <int ACT>
+__device__ __forceinline__ uint32_t act_pack2(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  if constexpr (ACT == SMLRT_RELU) return pack_relu_bf16(lo, hi);
+  else if constexpr (ACT == SMLRT_TANH) return pack_bf16(tanhf(lo), tanhf(hi));
+  else return pack_bf16(lo, hi);
+}
+
+// Thread (rq, cq) of the 256 producer threads computes rows rq and rq + 64 of
+// the tile for k pairs [8 cq, 8 cq + 8) of each 64-wide chunk: every
+// broadcast weight load (LDS.128) serves two rows, halving the producer's
+// share of the SMEM port the tensor core reads its operands through.
+template <int ACT1, int F>
+__device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n_my, const L12Args& a,
+                                             const DevPlan& Pin, int tid) {
+  using L = L12Lay<1>;  // A ring / W1 offsets do not depend on NH
+  const int KB = a.H1 / 64;
+  const int rq = tid & 63, cq = tid >> 6;
+  const uint32_t w1s = smem_u32(smem + L::OFF_W1);  // explicit ld.shared (a generic load stalls on long scoreboard)
+  // the next tile's inputs are loaded one tile ahead (DRAM latency off the A ring's critical path)
+  auto load_x = [&](int i, float (&x)[2][F]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t m = (int64_t)(blockIdx.x + i * gridDim.x) * GBM + rq + 64 * h;
+      const int64_t ro = m < a.M ? row_offset_uniform(Pin, (uint32_t)(a.r0 + m)) : 0;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        x[h][f] = 0.0f;
+        if (m < a.M && f < a.F && i < n_my) {
+          const int64_t addr = Pin.col_inl[f] + ro;
+          x[h][f] = a.src_dt == SMLRT_F32 ? __ldg(reinterpret_cast<const float*>(a.src) + addr)
+                                          : __double2float_rn(__ldg(reinterpret_cast<const double*>(a.src) + addr));
+        }
+      }
+    }
+  };
+  float xn[2][F];
+  load_x(0, xn);
+  int s = 0, ph = 0;
+  for (int i = 0; i < n_my; ++i) {
+    uint64_t xd[2][F];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const float x = __bfloat162float(__float2bfloat16_rn(xn[h][f]));  // the tensor-core operand precision
+        xd[h][f] = f2pk(x, x);
+      }
+    load_x(i + 1, xn);
+    for (int kb = 0; kb < KB; ++kb) {
+      mbar_wait(bar + L::AEMPTY + s, ph ^ 1);
+      const uint32_t ab = smem_u32(smem + L::OFF_A) + s * L::A_BYTES;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {  // 16-byte chunk j = k pairs 4j..4j+3
+        const int j = 2 * cq + jj;
+        uint32_t pk[2][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t w = w1s + (uint32_t)(kb * 32 + 4 * j + q) * 64;
+          const float4 w0 = ld_shared_f4(w), w1 = ld_shared_f4(w + 16), w2 = ld_shared_f4(w + 32),
+                       w3 = ld_shared_f4(w + 48);
+          const float wv[14] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w, w3.x, w3.y};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint64_t acc = f2pk(w3.z, w3.w);  // (b1[k], b1[k+1])
+#pragma unroll
+            for (int f = 0; f < F; ++f) acc = ffma2(xd[h][f], f2pk(wv[2 * f], wv[2 * f + 1]), acc);
+            pk[h][q] = act_pack2<ACT1>(acc);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = rq + 64 * h;
+          st_shared_v4(ab + r * 128 + ((j ^ (r & 7)) << 4), pk[h][0], pk[h][1], pk[h][2], pk[h][3]);  // SW128
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(bar + L::AFULL + s);
+      if (++s == L12_SA) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  }
+}
+
+// thread = row of this warp's lane quarter; this warp group drains N-half h
+// with the next 16-column TMEM load in flight while the current one is
+// converted and stored
+template <int ACT2, int NH>
+__device__ __forceinline__ void l12_epilogue(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my,
+                                             const L12Args& a, int q, int h, int lane) {
+  using L = L12Lay<NH>;
+  const int r = q * 32 + lane;
+  const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + h * 256;
+  const uint32_t b2s = smem_u32(smem + L::OFF_B2) + h * 256 * 4;
+  for (int i = 0; i < n_my; ++i) {
+    const int64_t m = (int64_t)(blockIdx.x + i * gridDim.x) * GBM + r;
+    mbar_wait_sleep(bar + L::TFULL, i & 1);
+    tc_fence_after();
+    uint4* o = reinterpret_cast<uint4*>(a.out + m * (NH * 256) + h * 256);
+    uint32_t v[2][16];
+    tmem_ld16(taddr, v[0]);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      tmem_wait_ld16(v[c & 1]);
+      if (c + 1 < 16) {
+        tmem_ld16(taddr + (c + 1) * 16, v[(c + 1) & 1]);
+      } else {
+        tc_fence_before();
+        mbar_arrive(bar + L::TEMPTY + h);
+      }
+      uint32_t p[8];
+#pragma unroll
+      for (int e4 = 0; e4 < 4; ++e4) {
+        const float4 bb = ld_shared_f4(b2s + (c * 16 + 4 * e4) * 4);
+        const uint32_t* vv = v[c & 1] + 4 * e4;
+        p[2 * e4] = pack_bf16(act_g<ACT2>(__uint_as_float(vv[0]) + bb.x), act_g<ACT2>(__uint_as_float(vv[1]) + bb.y));
+        p[2 * e4 + 1] =
+            pack_bf16(act_g<ACT2>(__uint_as_float(vv[2]) + bb.z), act_g<ACT2>(__uint_as_float(vv[3]) + bb.w));
+      }
+      if (m < a.M) {
+        o[2 * c] = make_uint4(p[0], p[1], p[2], p[3]);
+        o[2 * c + 1] = make_uint4(p[4], p[5], p[6], p[7]);
+      }
+    }
+  }
+}
+
+template <int NH, int F>
+__global__ void __launch_bounds__(l12_threads<NH>(), 1)
+    l12_fused_kernel(const __grid_constant__ CUtensorMap tb, const __grid_constant__ L12Args a,
+                     const __grid_constant__ DevPlan Pin) {
+  using L = L12Lay<NH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+  const int n_tiles = (a.M + GBM - 1) / GBM;
+  const int n_my = (int)blockIdx.x < n_tiles ? (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int KB = a.H1 / 64;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < L12_SA; ++i) {
+      mbar_init(bar + L::AFULL + i, 32 * L12_PW);
+      mbar_init(bar + L::AEMPTY + i, 1);
+    }
+    for (int i = 0; i < L12_SB; ++i) {
+      mbar_init(bar + L::BFULL + i, 1);
+      mbar_init(bar + L::BEMPTY + i, 1);
+    }
+    mbar_init(bar + L::TFULL, 1);
+    for (int h = 0; h < NH; ++h) mbar_init(bar + L::TEMPTY + h, 128);  // one warp group per half
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+  }
+  {
+    const float4* g = reinterpret_cast<const float4*>(a.w1p);
+    float4* w = reinterpret_cast<float4*>(smem + L::OFF_W1);
+    for (int i = threadIdx.x; i < a.H1 / 2 * 4; i += l12_threads<NH>()) w[i] = g[i];
+    float* b2s = reinterpret_cast<float*>(smem + L::OFF_B2);
+    for (int i = threadIdx.x; i < NH * 256; i += l12_threads<NH>()) b2s[i] = a.b2[i];
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0, ph = 0;
+      for (int i = 0; i < n_my; ++i)
+        for (int kb = 0; kb < KB; ++kb)
+          for (int h = 0; h < NH; ++h) {
+            mbar_wait(bar + L::BEMPTY + s, ph ^ 1);
+            mbar_expect_tx(bar + L::BFULL + s, L::B_BYTES);
+            tma_load_2d(smem_u32(smem + L::OFF_B + s * L::B_BYTES), &tb, bar + L::BFULL + s, kb * 64, h * 256);
+            if (++s == L12_SB) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(GBM, 256);
+      const uint64_t a0 = smem_desc(smem_u32(smem + L::OFF_A), 1024, kSwizzle128);
+      const uint64_t b0 = smem_desc(smem_u32(smem + L::OFF_B), 1024, kSwizzle128);
+      int sa = 0, pa = 0, sb = 0, pb = 0;
+      for (int i = 0; i < n_my; ++i) {
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(bar + L::AFULL + sa, pa);
+          tc_fence_after();
+          for (int h = 0; h < NH; ++h) {
+            mbar_wait(bar + L::BFULL + sb, pb);
+            if (kb == 0) mbar_wait(bar + L::TEMPTY + h, (i & 1) ^ 1);
+            tc_fence_after();
+            const uint64_t ad = a0 + ((sa * L::A_BYTES) >> 4);
+            const uint64_t bd = b0 + ((sb * L::B_BYTES) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_bf16(tbase + h * 256, ad + k * 2, bd + k * 2, idesc, (kb | k) != 0);
+            mma_commit(bar + L::BEMPTY + sb);
+            if (++sb == L12_SB) {
+              sb = 0;
+              pb ^= 1;
+            }
+          }
+          mma_commit(bar + L::AEMPTY + sa);
+          if (++sa == L12_SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+        }
+        mma_commit(bar + L::TFULL);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + 4 * NH) {
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    if (a.act2 == SMLRT_RELU)
+      l12_epilogue<SMLRT_RELU, NH>(smem, bar, tbase, n_my, a, q, h, lane);
+    else if (a.act2 == SMLRT_TANH)
+      l12_epilogue<SMLRT_TANH, NH>(smem, bar, tbase, n_my, a, q, h, lane);
+    else
+      l12_epilogue<SMLRT_IDENTITY, NH>(smem, bar, tbase, n_my, a, q, h, lane);
+  } else {
+    const int t = threadIdx.x - 32 * (2 + 4 * NH);
+    if (a.act1 == SMLRT_RELU)
+      l12_producer<SMLRT_RELU, F>(smem, bar, n_my, a, Pin, t);
+    else if (a.act1 == SMLRT_TANH)
+      l12_producer<SMLRT_TANH, F>(smem, bar, n_my, a, Pin, t);
+    else
+      l12_producer<SMLRT_IDENTITY, F>(smem, bar, n_my, a, Pin, t);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -382,6 +687,15 @@ uint16_t bf16_bits(float f) {
 // --------------------------------------------------------- wide MLP models
 // dense 4-layer models F(<=16) -> H1 (multiple of 256) -> H2 (multiple of 64,
 // <=1024) -> H3 (<= 256, multiple of 32) -> 1
+// SMLRT_WIDE_UNFUSED=1: materialise layer 1 (A/B measurements, parity tests of both paths)
+bool l12_disabled() {
+  static const int v = [] {
+    const char* e = std::getenv("SMLRT_WIDE_UNFUSED");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 bool wide_shape(const smlrt_model_s& m) {
   if (m.n_layers != 4) return false;
   for (const auto& L : m.layers)
@@ -391,8 +705,21 @@ bool wide_shape(const smlrt_model_s& m) {
          h3 % 32 == 0 && h3 <= 256 && m.layers[3].out == 1 && h1 % 64 == 0;
 }
 
+// layers 1+2 fused on chip (l12_fused_kernel): F <= 7, H1 <= 1024, H2 in {256, 512}
+bool l12_shape(const smlrt_model_s& m) {
+  const int h1 = m.layers[0].out, h2 = m.layers[1].out;
+  return m.in_features <= 7 && h1 <= L12_H1MAX && h1 % 64 == 0 && (h2 == 256 || h2 == 512);
+}
+
+size_t wide_w1p_off(const smlrt_model_s& m) {  // byte offset of the f32 layer-1 pair table in tc_blob
+  const int h1 = m.layers[0].out, h2 = m.layers[1].out, h3 = m.layers[2].out;
+  const size_t bf = ((size_t)h1 * 16 + (size_t)h2 * h1 + (size_t)h3 * h2) * 2;
+  return (bf + 255) & ~size_t(255);
+}
+
 int wide_pack(smlrt_model_s& m) {
-  // bf16 weights: W1p [H1][16] (K padded), W2 [H2][H1], W3 [H3][H2]
+  // bf16 weights: W1p [H1][16] (K padded), W2 [H2][H1], W3 [H3][H2]; then (l12
+  // shapes) the f32 layer-1 pair table of l12_fused_kernel
   const int F = m.in_features, h1 = m.layers[0].out, h2 = m.layers[1].out, h3 = m.layers[2].out;
   std::vector<uint16_t> w((size_t)h1 * 16 + (size_t)h2 * h1 + (size_t)h3 * h2, 0);
   const float* p = m.host_params.data();
@@ -404,9 +731,50 @@ int wide_pack(smlrt_model_s& m) {
     for (int k = 0; k < 16; ++k) w[o++] = k < F ? bf16_bits(W1[(size_t)n * F + k]) : 0;
   for (size_t i = 0; i < (size_t)h2 * h1; ++i) w[o++] = bf16_bits(W2[i]);
   for (size_t i = 0; i < (size_t)h3 * h2; ++i) w[o++] = bf16_bits(W3[i]);
-  SMLRT_CUDA(cudaMalloc(&m.tc_blob, w.size() * 2));
+  const size_t off = wide_w1p_off(m);
+  std::vector<float> pairs;
+  if (l12_shape(m)) {
+    const float* b1 = W1 + (size_t)h1 * F;
+    auto bfv = [](float v) {  // value of the bf16 rounding of v
+      uint32_t u = (uint32_t)bf16_bits(v) << 16;
+      float r;
+      std::memcpy(&r, &u, 4);
+      return r;
+    };
+    pairs.assign((size_t)h1 / 2 * 16, 0.0f);
+    for (int p = 0; p < h1 / 2; ++p) {
+      for (int f = 0; f < F; ++f) {
+        pairs[(size_t)p * 16 + 2 * f] = bfv(W1[(size_t)(2 * p) * F + f]);
+        pairs[(size_t)p * 16 + 2 * f + 1] = bfv(W1[(size_t)(2 * p + 1) * F + f]);
+      }
+      pairs[(size_t)p * 16 + 14] = b1[2 * p];
+      pairs[(size_t)p * 16 + 15] = b1[2 * p + 1];
+    }
+  }
+  const size_t bytes = pairs.empty() ? w.size() * 2 : off + pairs.size() * 4;
+  SMLRT_CUDA(cudaMalloc(&m.tc_blob, bytes));
   SMLRT_CUDA(cudaMemcpy(m.tc_blob, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
-  m.tc_bytes = w.size() * 2;
+  if (!pairs.empty())
+    SMLRT_CUDA(cudaMemcpy(reinterpret_cast<uint8_t*>(m.tc_blob) + off, pairs.data(), pairs.size() * 4,
+                          cudaMemcpyHostToDevice));
+  m.tc_bytes = bytes;
+  return SMLRT_OK;
+}
+
+template <int NH, int F>
+int l12_launch(const CUtensorMap& tb, const L12Args& a, const DevPlan& in, cudaStream_t s) {
+  using L = L12Lay<NH>;
+  static int configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1 << dev))) {
+    SMLRT_CUDA(cudaFuncSetAttribute(l12_fused_kernel<NH, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC));
+    configured |= 1 << dev;
+  }
+  const int tiles = (a.M + GBM - 1) / GBM;
+  const int grid = std::max(1, std::min(tiles, sm_count()));
+  l12_fused_kernel<NH, F><<<grid, l12_threads<NH>(), L::ALLOC, s>>>(tb, a, in);
+  SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
 
@@ -420,11 +788,18 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
   const __nv_bfloat16* W3 = W2 + (size_t)h2 * h1;
   const int64_t rows = r1 - r0;
   const int64_t ch = std::min<int64_t>(rows, 1 << 20);
+  const bool fused12 = l12_shape(m) && in.n_cols == F && F <= SMLRT_INLINE_COLS && !l12_disabled();
   __nv_bfloat16* buf;
-  SMLRT_CUDA(cudaMallocAsync(&buf, (size_t)ch * (16 + h1 + h2) * 2, s));
+  SMLRT_CUDA(cudaMallocAsync(&buf, (size_t)ch * (fused12 ? h2 : 16 + h1 + h2) * 2, s));
   __nv_bfloat16* x16 = buf;
   __nv_bfloat16* a1 = x16 + ch * 16;
-  __nv_bfloat16* a2 = a1 + ch * h1;
+  __nv_bfloat16* a2 = fused12 ? buf : a1 + ch * h1;
+  CUtensorMap tw2;
+  if (fused12)
+    if (int rc = make_map(&tw2, W2, h2, h1, h1, 256, 64)) {
+      cudaFreeAsync(buf, s);
+      return rc;
+    }
   OutPtrs dst{};
   for (int i = 0; i < n_out && i < 8; ++i) {
     dst.p[i] = out_ptrs[i];
@@ -434,29 +809,50 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
   int rc = SMLRT_OK;
   for (int64_t r = r0; r < r1 && !rc; r += ch) {
     const int n = (int)std::min(ch, r1 - r);
-    gather_bf16_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, in_ptrs[in.uarray], in_dt[in.uarray], F, r, n, x16);
-    if (cudaGetLastError() != cudaSuccess) return fail(SMLRT_E_CUDA, "gather_bf16 launch failed");
     GemmArgs g{};
     g.M = n;
     g.status = status;
-    // layer 1: [n x 16] * W1p^T -> a1 [n x h1]
-    g.N = h1;
-    g.K = 16;
-    g.act = m.layers[0].act;
-    g.bias = m.layers[0].b;
-    g.out = a1;
-    g.ldo = h1;
-    rc = gemm_launch<256, 16, 8, EPI_BF16>(x16, 16, W1p, 16, g, none, dst, s);
-    if (rc) break;
-    // layer 2: a1 * W2^T -> a2 [n x h2]
-    g.N = h2;
-    g.K = h1;
-    g.act = m.layers[1].act;
-    g.bias = m.layers[1].b;
-    g.out = a2;
-    g.ldo = h2;
-    rc = gemm_launch<256, 64, 4, EPI_BF16>(a1, h1, W2, h1, g, none, dst, s);
-    if (rc) break;
+    if (fused12) {
+      // layers 1 + 2 in one kernel, layer 1 produced on chip -> a2 [n x h2]
+      L12Args la{};
+      la.M = n;
+      la.H1 = h1;
+      la.F = F;
+      la.act1 = m.layers[0].act;
+      la.act2 = m.layers[1].act;
+      la.r0 = r;
+      la.w1p = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(m.tc_blob) + wide_w1p_off(m));
+      la.b2 = m.layers[1].b;
+      la.src = in_ptrs[in.uarray];
+      la.src_dt = in_dt[in.uarray];
+      la.out = a2;
+      if (h2 == 512)
+        rc = F <= 6 ? l12_launch<2, 6>(tw2, la, in, s) : l12_launch<2, 7>(tw2, la, in, s);
+      else
+        rc = F <= 6 ? l12_launch<1, 6>(tw2, la, in, s) : l12_launch<1, 7>(tw2, la, in, s);
+      if (rc) break;
+    } else {
+      gather_bf16_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, in_ptrs[in.uarray], in_dt[in.uarray], F, r, n, x16);
+      if (cudaGetLastError() != cudaSuccess) return fail(SMLRT_E_CUDA, "gather_bf16 launch failed");
+      // layer 1: [n x 16] * W1p^T -> a1 [n x h1]
+      g.N = h1;
+      g.K = 16;
+      g.act = m.layers[0].act;
+      g.bias = m.layers[0].b;
+      g.out = a1;
+      g.ldo = h1;
+      rc = gemm_launch<256, 16, 8, EPI_BF16>(x16, 16, W1p, 16, g, none, dst, s);
+      if (rc) break;
+      // layer 2: a1 * W2^T -> a2 [n x h2]
+      g.N = h2;
+      g.K = h1;
+      g.act = m.layers[1].act;
+      g.bias = m.layers[1].b;
+      g.out = a2;
+      g.ldo = h2;
+      rc = gemm_launch<256, 64, 4, EPI_BF16>(a1, h1, W2, h1, g, none, dst, s);
+      if (rc) break;
+    }
     // layer 3 + fused layer 4 (dot) + scatter
     g.N = h3;
     g.K = h2;

@@ -37,6 +37,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// try_wait with a suspend-time hint: a waiter with nothing else to do sleeps
+// until the phase completes instead of re-polling (each poll is an LSU op on
+// the shared-memory pipe the tensor core also reads its operands through)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tensor core, TMA)
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
