@@ -391,7 +391,7 @@ __device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n
       }
     load_x(i + 1, xn);
     for (int kb = 0; kb < KB; ++kb) {
-      mbar_wait(bar + L::AEMPTY + s, ph ^ 1);
+      mbar_wait_sleep(bar + L::AEMPTY + s, ph ^ 1);
       const uint32_t ab = smem_u32(smem + L::OFF_A) + s * L::A_BYTES;
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {  // 16-byte chunk j = k pairs 4j..4j+3
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(l12_threads<NH>(), 1)
       for (int i = 0; i < n_my; ++i)
         for (int kb = 0; kb < KB; ++kb)
           for (int h = 0; h < NH; ++h) {
-            mbar_wait(bar + L::BEMPTY + s, ph ^ 1);
+            mbar_wait_sleep(bar + L::BEMPTY + s, ph ^ 1);
             mbar_expect_tx(bar + L::BFULL + s, L::B_BYTES);
             tma_load_2d(smem_u32(smem + L::OFF_B + s * L::B_BYTES), &tb, bar + L::BFULL + s, kb * 64, h * 256);
             if (++s == L12_SB) {
