@@ -15,13 +15,15 @@
 // relu, 128->2) runs as front kernel + two tiled dense layers + scatter.
 #include <algorithm>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace smlrt {
 namespace {
 
 __device__ __forceinline__ float act_exact(float y, int act) {
-  if (act == SMLRT_RELU) return (y < 0.0f) ? 0.0f : y;
+  if (act == SMLRT_RELU) return (y > 0.0f || y != y) ? y : 0.0f;  // np.maximum(y, 0): NaN wins, -0 -> +0
   if (act == SMLRT_TANH) return tanhf(y);
   return y;
 }
@@ -189,6 +191,101 @@ __global__ void __launch_bounds__(256) conv_front_fixed_kernel(const __grid_cons
   }
 }
 
+// C4 front, specialised for one 1-channel frame per CTA with a 16 x 16
+// position grid (K = 8, OC = 8 over a 128 x 128 window), conv + act + 2x2
+// max-pool in registers: warp w owns conv rows 2w, 2w+1 (lane = 16 * row +
+// column), the pool is two butterfly shuffles.  Weights and bias ride in the
+// parameter bank (uniform LDCU into FMUL2 operands); output pairs (o, o+1)
+// accumulate with packed mul.rn.f32x2 + fma.rn.f32x2(p, 1, acc), the same
+// ordered multiply-then-add as the reference's _matmul_rowwise over the
+// (dy, dx) patch features -- bitwise equal, half the FP32 issue slots.
+struct ConvW8 {
+  float w[64 * 8];  // [(dy*8 + dx)][o]
+  float b[8];
+  uint64_t one2;    // (1.0f, 1.0f), opaque to ptxas (see kernels_simt.cu add2)
+};
+
+__device__ __forceinline__ uint64_t cpk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void cupk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t cmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t cadd2(uint64_t acc, uint64_t p, uint64_t one) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(p), "l"(one), "l"(acc));
+  return r;
+}
+
+__global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_constant__ FrontArgs a,
+                                                              const __grid_constant__ DevPlan P,
+                                                              const __grid_constant__ ConvW8 cw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int py = 2 * warp + (lane >> 4), px = lane & 15;
+  const int64_t row = a.r0 + blockIdx.x;
+  const float* img;
+  int64_t pitch;
+  if (a.x != nullptr) {
+    img = a.x + (row - a.r0) * (int64_t)a.H * a.W;
+    pitch = a.W;
+  } else {
+    img = reinterpret_cast<const float*>(a.src) + P.col_off0 + row_offset_uniform(P, (uint32_t)row);
+    pitch = P.win_pitch;
+  }
+  const float* prow = img + (int64_t)(py * 8) * pitch + px * 8;
+  float4 u[8][2];
+#pragma unroll
+  for (int dy = 0; dy < 8; ++dy) {  // all 16 loads in flight before the math
+    u[dy][0] = __ldg(reinterpret_cast<const float4*>(prow + dy * pitch));
+    u[dy][1] = __ldg(reinterpret_cast<const float4*>(prow + dy * pitch) + 1);
+  }
+  uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int dy = 0; dy < 8; ++dy) {
+    const float v[8] = {u[dy][0].x, u[dy][0].y, u[dy][0].z, u[dy][0].w,
+                        u[dy][1].x, u[dy][1].y, u[dy][1].z, u[dy][1].w};
+#pragma unroll
+    for (int dx = 0; dx < 8; ++dx) {
+      const uint64_t vv = cpk2(v[dx], v[dx]);
+      const float* wf = cw.w + (dy * 8 + dx) * 8;
+#pragma unroll
+      for (int op = 0; op < 4; ++op)
+        acc[op] = cadd2(acc[op], cmul2(vv, *reinterpret_cast<const uint64_t*>(wf + 2 * op)), cw.one2);
+    }
+  }
+  float y[8];
+#pragma unroll
+  for (int op = 0; op < 4; ++op) {
+    cupk2(cadd2(acc[op], *reinterpret_cast<const uint64_t*>(cw.b + 2 * op), cw.one2), y[2 * op], y[2 * op + 1]);
+    y[2 * op] = act_exact(y[2 * op], a.act);
+    y[2 * op + 1] = act_exact(y[2 * op + 1], a.act);
+  }
+  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  if (a.pool == 2) {
+    // 2x2 window = lanes {l, l^1, l^16, l^17}; NaN propagates like np.max
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      float m = max_nan(y[o], __shfl_xor_sync(0xffffffffu, y[o], 1));
+      m = max_nan(m, __shfl_xor_sync(0xffffffffu, m, 16));
+      y[o] = m;
+    }
+    if (lane < 16 && (lane & 1) == 0) {
+#pragma unroll
+      for (int o = 0; o < 8; ++o) orow[o * 64 + warp * 8 + (lane >> 1)] = y[o];
+    }
+  } else {
+#pragma unroll
+    for (int o = 0; o < 8; ++o) orow[o * 256 + py * 16 + px] = y[o];
+  }
+}
+
 // ------------------------------------------------------------ tiled dense --
 constexpr int TR = 64, TJ = 64, TK = 32;
 
@@ -289,7 +386,17 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
                        (P != nullptr && src_dt == SMLRT_F32 && P->win_w == a.W && P->win_pitch % 4 == 0 &&
                         ((P->col_off0 + P->ustride[0]) % 4 == 0) && P->n_sweep == 1 && P->col_off0 % 4 == 0 &&
                         (reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned) {
+  if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned && a.OH == 16 && a.OW == 16 && (a.pool == 1 || a.pool == 2) &&
+      m.host_params.size() >= 64 * 8 + 8) {
+    ConvW8 cw{};
+    const float* hw = m.host_params.data();  // conv layer first: W [OC][K*K], then b [OC]
+    for (int o = 0; o < 8; ++o)
+      for (int k = 0; k < 64; ++k) cw.w[k * 8 + o] = hw[o * 64 + k];
+    for (int o = 0; o < 8; ++o) cw.b[o] = hw[64 * 8 + o];
+    const float one[2] = {1.0f, 1.0f};
+    std::memcpy(&cw.one2, one, sizeof(one));
+    conv_pool_k8oc8_kernel<<<(unsigned)(r1 - r0), 256, 0, s>>>(a, P ? *P : dummy, cw);
+  } else if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned) {
     conv_front_fixed_kernel<8, 8><<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
   } else {
     conv_front_kernel<<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
