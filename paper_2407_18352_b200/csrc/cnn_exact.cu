@@ -287,57 +287,111 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------ tiled dense --
-constexpr int TR = 64, TJ = 64, TK = 32;
+// Exact dense layer on output pairs: thread = 4 rows x 4 columns (2 column
+// pairs), each multiply-accumulate a packed mul.rn.f32x2 + fma.rn.f32x2(p, 1,
+// acc) in ascending k -- the reference's ordered rowwise product, bitwise,
+// with half the FP32 issue slots of the scalar kernel above.  FUSE2 (out <=
+// 128, one column block): the layer's activations stay in shared memory and
+// the next dense layer (out2 <= 4 units, e.g. C4's 128 -> 2) runs in the
+// same CTA, one ordered dot product per (row, unit).
+constexpr int PR = 32, PJ = 128, PK = 32;
 
-__global__ void __launch_bounds__(256) dense_tiled_kernel(const float* __restrict__ x, int64_t rows, int in,
-                                                          int out, const float* __restrict__ W,
-                                                          const float* __restrict__ b, int act,
-                                                          float* __restrict__ y, uint32_t* status) {
-  __shared__ float xs[TK][TR + 4];
-  __shared__ float wsh[TK][TJ + 4];
-  const int tr = threadIdx.x / 16, tj = threadIdx.x % 16;  // 16 x 16 threads, 4 x 4 outputs each
-  const int64_t row0 = (int64_t)blockIdx.x * TR;
-  const int j0 = blockIdx.y * TJ;
-  float acc[4][4];
+template <bool FUSE2>
+__global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict__ x, int64_t rows, int in, int out,
+                                                         const float* __restrict__ W, const float* __restrict__ b,
+                                                         int act, float* __restrict__ y, uint32_t* status,
+                                                         const float* __restrict__ W2, const float* __restrict__ b2,
+                                                         int out2, int act2, uint64_t one) {
+  __shared__ __align__(16) float xs[PK][PR + 4];
+  __shared__ __align__(16) float wsh[PK][PJ + 4];
+  __shared__ float hs[FUSE2 ? PR : 1][FUSE2 ? PJ + 1 : 1];
+  const int tr = threadIdx.x >> 5, tj = threadIdx.x & 31;  // rows 4 tr .. +3, columns 4 tj .. +3
+  const int64_t row0 = (int64_t)blockIdx.x * PR;
+  const int j0 = blockIdx.y * PJ;
+  uint64_t acc[4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0ull;
+  // the next K tile is fetched into registers while the current one is consumed
+  constexpr int NX = PR * PK / 256, NW = PJ * PK / 256;
+  float px[NX], pw[NW];
+  auto fetch = [&](int k0) {
+    const int kn = min(PK, in - k0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-  for (int k0 = 0; k0 < in; k0 += TK) {
-    const int kn = min(TK, in - k0);
-    for (int i = threadIdx.x; i < TR * TK; i += 256) {
-      const int r = i / TK, k = i % TK;
+    for (int u = 0; u < NX; ++u) {
+      const int i = threadIdx.x + 256 * u, r = i / PK, k = i % PK;
       const int64_t gr = row0 + r;
-      xs[k][r] = (gr < rows && k < kn) ? x[gr * in + k0 + k] : 0.0f;
+      px[u] = (gr < rows && k < kn) ? x[gr * in + k0 + k] : 0.0f;
     }
-    for (int i = threadIdx.x; i < TJ * TK; i += 256) {
-      const int j = i / TK, k = i % TK;
-      wsh[k][j] = (j0 + j < out && k < kn) ? __ldg(W + (int64_t)(j0 + j) * in + k0 + k) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int i = threadIdx.x + 256 * u, j = i / PK, k = i % PK;
+      pw[u] = (j0 + j < out && k < kn) ? __ldg(W + (int64_t)(j0 + j) * in + k0 + k) : 0.0f;
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < in; k0 += PK) {
+    const int kn = min(PK, in - k0);
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      xs[i % PK][i / PK] = px[u];
+    }
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      wsh[i % PK][i / PK] = pw[u];
     }
     __syncthreads();
+    if (k0 + PK < in) fetch(k0 + PK);
     for (int k = 0; k < kn; ++k) {
       const float4 xv = *reinterpret_cast<const float4*>(&xs[k][tr * 4]);
       const float4 wv = *reinterpret_cast<const float4*>(&wsh[k][tj * 4]);
+      const uint64_t w01 = cpk2(wv.x, wv.y), w23 = cpk2(wv.z, wv.w);
       const float xr[4] = {xv.x, xv.y, xv.z, xv.w};
-      const float wr[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(xr[i], wr[j]));
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t xx = cpk2(xr[i], xr[i]);
+        acc[i][0] = cadd2(acc[i][0], cmul2(xx, w01), one);
+        acc[i][1] = cadd2(acc[i][1], cmul2(xx, w23), one);
+      }
     }
     __syncthreads();
   }
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int64_t r = row0 + tr * 4 + i;
+    const int rl = tr * 4 + i;
+    const int64_t r = row0 + rl;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = j0 + tj * 4 + j;
-      if (r < rows && c < out) {
-        const float v = act_exact(__fadd_rn(acc[i][j], __ldg(b + c)), act);
-        y[r * out + c] = v;
-        bad |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+    for (int p = 0; p < 2; ++p) {
+      float v[2];
+      cupk2(acc[i][p], v[0], v[1]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cl = tj * 4 + 2 * p + e, c = j0 + cl;
+        if (c < out) {
+          const float hv = act_exact(__fadd_rn(v[e], __ldg(b + c)), act);
+          if constexpr (FUSE2) {
+            hs[rl][cl] = hv;
+          } else if (r < rows) {
+            y[r * out + c] = hv;
+            bad |= (__float_as_uint(hv) & 0x7f800000u) == 0x7f800000u;
+          }
+        }
+      }
+    }
+  }
+  if constexpr (FUSE2) {
+    __syncthreads();
+    if ((int)threadIdx.x < PR * out2) {
+      const int rl = threadIdx.x / out2, o = threadIdx.x % out2;
+      const int64_t r = row0 + rl;
+      float a2 = 0.0f;
+      for (int f = 0; f < out; ++f) a2 = __fadd_rn(a2, __fmul_rn(hs[rl][f], __ldg(W2 + o * out + f)));
+      const float yv = act_exact(__fadd_rn(a2, __ldg(b2 + o)), act2);
+      if (r < rows) {
+        y[r * out2 + o] = yv;
+        bad = (__float_as_uint(yv) & 0x7f800000u) == 0x7f800000u;
       }
     }
   }
@@ -406,8 +460,26 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
 }
 
 // dense tail (layers [first, n)) over front output; ping-pong through t0/t1
+uint64_t one2() {
+  const float one[2] = {1.0f, 1.0f};
+  uint64_t v;
+  std::memcpy(&v, one, sizeof(v));
+  return v;
+}
+
 int dense_tail(const smlrt_model_s& m, int first, const float* cur, int64_t rows, float* y, float* t0, float* t1,
                cudaStream_t s, uint32_t* status) {
+  if (rows <= 0) return SMLRT_OK;
+  // common CNN tail: dense (<= 128 units) -> dense (<= 4 units), fused in one launch
+  if (m.n_layers - first == 2 && m.layers[first].kind == SMLRT_DENSE && m.layers[first + 1].kind == SMLRT_DENSE &&
+      m.layers[first].out <= PJ && m.layers[first + 1].out <= 4) {
+    const DevLayer &L1 = m.layers[first], &L2 = m.layers[first + 1];
+    dim3 grid((unsigned)((rows + PR - 1) / PR), 1);
+    dense_pair_kernel<true><<<grid, 256, 0, s>>>(cur, rows, L1.in, L1.out, L1.w, L1.b, L1.act, y, status, L2.w, L2.b,
+                                                  L2.out, L2.act, one2());
+    SMLRT_CUDA(cudaGetLastError());
+    return SMLRT_OK;
+  }
   for (int l = first; l < m.n_layers; ++l) {
     const bool last = l == m.n_layers - 1;
     float* dst = last ? y : ((l - first) % 2 ? t1 : t0);
@@ -431,8 +503,9 @@ int launch_dense_exact_tiled(const float* x, int64_t rows, const DevLayer& L, fl
                              uint32_t* status) {
   if (rows <= 0) return SMLRT_OK;
   if (L.kind != SMLRT_DENSE) return fail(SMLRT_E_UNSUPPORTED, "layer order not supported by the exact path");
-  dim3 grid((unsigned)((rows + TR - 1) / TR), (unsigned)((L.out + TJ - 1) / TJ));
-  dense_tiled_kernel<<<grid, 256, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status);
+  dim3 grid((unsigned)((rows + PR - 1) / PR), (unsigned)((L.out + PJ - 1) / PJ));
+  dense_pair_kernel<false><<<grid, 256, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status, nullptr, nullptr, 0,
+                                                SMLRT_IDENTITY, one2());
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
