@@ -220,6 +220,7 @@ def run_ours(args, rank, world, local):
 
     rt.kernel_events.clear()
     step_events = []
+    launches0 = _native.launch_count()
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -234,6 +235,7 @@ def run_ours(args, rank, world, local):
             step_events.append((e0, e1))
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
+    launches = _native.launch_count() - launches0
     barrier(world)
     ms_steps = sum(a.elapsed_time(b) for a, b in step_events)
     ms_kernel = [a.elapsed_time(b) for a, b in rt.kernel_events]
@@ -249,7 +251,12 @@ def run_ours(args, rank, world, local):
     hbm_gbs = wl.elements * spec.bytes_per_elem / (k_ms / 1e3) / 1e9
     tflops = wl.elements * spec.flops_per_elem / (k_ms / 1e3) / 1e12
     if spec.precision == "bf16":
-        cpeak, cname = pk["bf16_tflops"], f"bf16_tflops ({pk_src}, burst)"
+        # burst figure for a kernel timed alone; the sustained (power-capped)
+        # one for a long step (the wide C3 path runs ~100 ms per step)
+        if k_ms > 20.0 and "bf16_tflops_sustained" in pk:
+            cpeak, cname = pk["bf16_tflops_sustained"], f"bf16_tflops_sustained ({pk_src}, long step)"
+        else:
+            cpeak, cname = pk["bf16_tflops"], f"bf16_tflops ({pk_src}, burst)"
     else:
         cpeak, cname = FP32_NOFMA_TFLOPS_AT_MAX, "FP32 CUDA-core mul+add issue rate at 1965 MHz (no FMA: exact path)"
     f_hbm, f_cmp = hbm_gbs / pk["hbm_gbs"], tflops / cpeak
@@ -316,7 +323,7 @@ def run_ours(args, rank, world, local):
                    "parallelism": f"dp{world} (sweep shards, no collective)",
                    "l2": "flushed between steps" if flush is not None else "inputs larger than L2"},
         "roofline": roof, "e2e": e2e, "cpu_baseline": cpu,
-        "gpu_launches": len(ms_kernel),
+        "gpu_launches": launches,
         "clocks": clk.summary(),
         "wall_s": round(t_wall, 3),
     }

@@ -113,6 +113,9 @@ typedef struct {
 
 const char* smlrt_version(void);
 const char* smlrt_last_error(void);
+/* Number of CUDA kernels this library has launched since it was loaded
+ * (instrumentation: the bench reports its own launches per timed region). */
+unsigned long long smlrt_launch_count(void);
 
 /*
  * Plan compiler.  Replaces the per-call extract/resolve/wrap + np.unique of

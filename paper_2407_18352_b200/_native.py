@@ -77,6 +77,7 @@ _I64 = C.c_int64
 SIGNATURES = {
     "smlrt_version": (C.c_char_p, []),
     "smlrt_last_error": (C.c_char_p, []),
+    "smlrt_launch_count": (C.c_ulonglong, []),
     "smlrt_plan_create": (_I, [C.POINTER(View), _I, _I, C.POINTER(_I64), _I, C.POINTER(_I64), _I,
                                C.POINTER(_P)]),
     "smlrt_plan_info": (_I, [_P, C.POINTER(PlanInfo)]),
@@ -143,6 +144,11 @@ def _arr(ctype, values):
 
 def version() -> str:
     return lib().smlrt_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels this library has launched since load (bench instrumentation)."""
+    return int(lib().smlrt_launch_count())
 
 
 # ------------------------------------------------------------------ plans --

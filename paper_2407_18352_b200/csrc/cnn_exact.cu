@@ -450,10 +450,13 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
     const float one[2] = {1.0f, 1.0f};
     std::memcpy(&cw.one2, one, sizeof(one));
     conv_pool_k8oc8_kernel<<<(unsigned)(r1 - r0), 256, 0, s>>>(a, P ? *P : dummy, cw);
+    count_launch();
   } else if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned) {
     conv_front_fixed_kernel<8, 8><<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
+    count_launch();
   } else {
     conv_front_kernel<<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
+    count_launch();
   }
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
@@ -477,6 +480,7 @@ int dense_tail(const smlrt_model_s& m, int first, const float* cur, int64_t rows
     dim3 grid((unsigned)((rows + PR - 1) / PR), 1);
     dense_pair_kernel<true><<<grid, 256, 0, s>>>(cur, rows, L1.in, L1.out, L1.w, L1.b, L1.act, y, status, L2.w, L2.b,
                                                   L2.out, L2.act, one2());
+    count_launch();
     SMLRT_CUDA(cudaGetLastError());
     return SMLRT_OK;
   }
@@ -506,6 +510,7 @@ int launch_dense_exact_tiled(const float* x, int64_t rows, const DevLayer& L, fl
   dim3 grid((unsigned)((rows + PR - 1) / PR), (unsigned)((L.out + PJ - 1) / PJ));
   dense_pair_kernel<false><<<grid, 256, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status, nullptr, nullptr, 0,
                                                 SMLRT_IDENTITY, one2());
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -144,6 +145,11 @@ struct smlrt_plan_s {
 };
 
 namespace smlrt {
+
+// kernels launched by this library since load (smlrt_launch_count): the bench
+// reports how many of its own launches a timed region made
+extern std::atomic<unsigned long long> g_launches;
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // one dense layer on the device
 struct DevLayer {

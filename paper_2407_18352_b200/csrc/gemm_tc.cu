@@ -643,6 +643,7 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, const Ge
   const int tiles = ((g.M + GBM - 1) / GBM) * ((g.N + BN - 1) / BN);
   const int grid = std::max(1, std::min(tiles, sm_count()));
   gemm_tc_kernel<BN, BK, STAGES, EPI><<<grid, GTHREADS, L::ALLOC, s>>>(ta, tb, g, Pout, dst);
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -774,6 +775,7 @@ int l12_launch(const CUtensorMap& tb, const L12Args& a, const DevPlan& in, cudaS
   const int tiles = (a.M + GBM - 1) / GBM;
   const int grid = std::max(1, std::min(tiles, sm_count()));
   l12_fused_kernel<NH, F><<<grid, l12_threads<NH>(), L::ALLOC, s>>>(tb, a, in);
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -833,6 +835,7 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
       if (rc) break;
     } else {
       gather_bf16_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, in_ptrs[in.uarray], in_dt[in.uarray], F, r, n, x16);
+      count_launch();
       if (cudaGetLastError() != cudaSuccess) return fail(SMLRT_E_CUDA, "gather_bf16 launch failed");
       // layer 1: [n x 16] * W1p^T -> a1 [n x h1]
       g.N = h1;

@@ -592,6 +592,7 @@ int try_fused(const smlrt_model_s& m, const DevPlan& in, const Ptrs& src, const 
     go(std::integral_constant<int, SMLRT_RELU>{});
   else
     go(std::integral_constant<int, SMLRT_TANH>{});
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -609,6 +610,7 @@ int launch_gather(const DevPlan& p, const void* const* ptrs, const int32_t* dtyp
     gather_kernel<float><<<grid_for(n), kThreads, 0, s>>>(p, src, (float*)out, r0, n);
   else
     gather_kernel<double><<<grid_for(n), kThreads, 0, s>>>(p, src, (double*)out, r0, n);
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -623,6 +625,7 @@ int launch_scatter(const DevPlan& p, const void* in, int in_dtype, void* const* 
     scatter_kernel<float><<<grid_for(n), kThreads, 0, s>>>(p, (const float*)in, dst, r0, n, gate);
   else
     scatter_kernel<double><<<grid_for(n), kThreads, 0, s>>>(p, (const double*)in, dst, r0, n, gate);
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -633,6 +636,7 @@ int launch_dense_exact(const float* x, int64_t rows, const DevLayer& L, float* y
   constexpr int TJ = 8;
   dim3 grid((unsigned)((rows + kThreads - 1) / kThreads), (unsigned)((L.out + TJ - 1) / TJ));
   dense_exact_kernel<TJ><<<grid, kThreads, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status);
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }
@@ -647,6 +651,7 @@ int launch_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cuda
     convert_kernel<double, float><<<grid_for(n), kThreads, 0, s>>>((const double*)src, (float*)dst, n);
   else
     convert_kernel<float, double><<<grid_for(n), kThreads, 0, s>>>((const float*)src, (double*)dst, n);
+  count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
 }

@@ -715,6 +715,7 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
   if (!pair) {
     const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
     mlp3_tc_kernel<H1, H2, false><<<grid, NTHREADS, Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
+    count_launch();
   } else {
     const int pairs = (a.n_tiles + 1) / 2;
     const int grid = 2 * std::max(1, std::min(pairs, num_sms() / 2));
@@ -731,6 +732,7 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     cfg.attrs = at;
     cfg.numAttrs = 1;
     SMLRT_CUDA(cudaLaunchKernelEx(&cfg, mlp3_tc_kernel<H1, H2, true>, a, in, src, out, dst));
+    count_launch();
   }
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;

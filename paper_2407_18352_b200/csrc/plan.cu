@@ -48,6 +48,11 @@ using namespace smlrt;
 extern "C" const char* smlrt_last_error(void) { return g_err.c_str(); }
 extern "C" const char* smlrt_version(void) { return "smlrt_b200 0.1.0 (sm_100a)"; }
 
+namespace smlrt {
+std::atomic<unsigned long long> g_launches{0};
+}
+extern "C" unsigned long long smlrt_launch_count(void) { return smlrt::g_launches.load(); }
+
 smlrt_plan_s::~smlrt_plan_s() {
   int prev = 0;
   cudaGetDevice(&prev);
