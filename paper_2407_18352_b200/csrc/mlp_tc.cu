@@ -97,7 +97,19 @@ struct TcArgs {
   int n_tiles;
   float* staged;
   uint32_t* status;
+  // biases and the last layer's weights in the parameter bank (uniform LDCU
+  // in the epilogues; the single-CTA kernel adds the biases there instead of
+  // spending tensor-core K slices and shared-memory bandwidth on them)
+  alignas(16) float b1[256];
+  float b2[256];
+  float w3[256];
 };
+
+__device__ __forceinline__ uint64_t add2f(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 struct Ptrs8 {
   const void* p[8];
@@ -169,7 +181,7 @@ __device__ __forceinline__ void arrive_mma(uint64_t* bar) {
 // warpgroup covers columns [half*H1/2, (half+1)*H1/2).
 template <int ACT, int H1, int H2, class L, bool PAIR>
 __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int half,
-                                          int q, int lane) {
+                                          int q, int lane, const TcArgs& a) {
   constexpr int HC = H1 / 2;
   const int r = q * 32 + lane;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L1 + half * HC;
@@ -201,6 +213,16 @@ __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t
         if (q == 0 && half == 0 && lane == 0) TR(4, it);
       }
       const float* f = reinterpret_cast<const float*>(v[c & 1]);
+      float fb[16];
+      if constexpr (!PAIR) {  // + b1 (packed adds, bias pairs from the parameter bank)
+        const uint64_t* bp = reinterpret_cast<const uint64_t*>(a.b1 + half * HC + c * 16);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint64_t sum = add2f(*reinterpret_cast<const uint64_t*>(&v[c & 1][2 * e]), bp[e]);
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(fb[2 * e]), "=f"(fb[2 * e + 1]) : "l"(sum));
+        }
+        f = fb;
+      }
       const uint32_t coff = boff + (c >> 2) * L::A2_CHUNK;
 #pragma unroll
       for (int j = 0; j < 2; ++j)
@@ -244,6 +266,15 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
       }
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
+        if constexpr (!PAIR) {
+          const float4 ww = *reinterpret_cast<const float4*>(a.w3 + cc * 32 + e);
+          const float4 bb = *reinterpret_cast<const float4*>(a.b2 + cc * 32 + e);
+          acc[((e >> 2) & 1) * 4 + 0] = fmaf(act_t<ACT>(__uint_as_float(v[e]) + bb.x), ww.x, acc[((e >> 2) & 1) * 4 + 0]);
+          acc[((e >> 2) & 1) * 4 + 1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1]) + bb.y), ww.y, acc[((e >> 2) & 1) * 4 + 1]);
+          acc[((e >> 2) & 1) * 4 + 2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2]) + bb.z), ww.z, acc[((e >> 2) & 1) * 4 + 2]);
+          acc[((e >> 2) & 1) * 4 + 3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3]) + bb.w), ww.w, acc[((e >> 2) & 1) * 4 + 3]);
+          continue;
+        }
         const float4 ww = ld_shared_f4(w3 + (cc * 32 + e) * 4);
         acc[((e >> 2) & 1) * 4 + 0] = fmaf(act_t<ACT>(__uint_as_float(v[e])), ww.x, acc[((e >> 2) & 1) * 4 + 0]);
         acc[((e >> 2) & 1) * 4 + 1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1])), ww.y, acc[((e >> 2) & 1) * 4 + 1]);
@@ -426,6 +457,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
       }
     }
+  } else if (warp == WARP_MMA && !PAIR) {
+    // ========================================================= MMA issuer
+    // Whole warp runs the loop (warp-uniform control flow, descriptors in
+    // uniform registers), elect.sync inside the asm picks the issuing lane:
+    // ~3 instructions per MMA.  A lane-0 branch costs ~14 (R2UR / ELECT /
+    // BRA.U.ANY per MMA), ~110 cycles of single-warp issue latency -- more
+    // than the 64 tensor cycles of an M=128 N=128 K=16 MMA, which made the
+    // issuer the bottleneck.
+    constexpr uint32_t idesc1 = idesc_bf16(BM, H1);
+    constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
+    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
+    const uint64_t x0d = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
+    const uint64_t a20d = smem_desc(smem_u32(smem + L::OFF_A2), 1024, kSwizzle128);
+    const uint64_t w20d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
+    auto issue_l2 = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
+      if (lane == 0) TR(11, j);
+      mbar_wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
+      if (lane == 0) TR(1, j);
+      tc_fence_after();
+      const uint32_t d = tbase + L::T_L2 + b * H2;
+      const uint64_t ab = a20d + ((b * L::A2_BUF) >> 4);
+#pragma unroll
+      for (int kc = 0; kc < L::KC; ++kc)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_ss_elect(d, ab + ((kc * L::A2_CHUNK + k * 32) >> 4), w20d + ((kc * L::W2_CHUNK + k * 32) >> 4), idesc2,
+                       (kc | k) != 0);
+      mma_commit_elect(bar + L::B_A2EMPTY + b);
+      mma_commit_elect(bar + L::B_L2FULL + b);
+    };
+    for (int it = 0; it < n_my; ++it) {
+      const int s = it % XSTAGES;
+      mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
+      if (lane == 0) TR(9, it);
+      mbar_wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
+      if (lane == 0) TR(0, it);
+      tc_fence_after();
+      mma_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d, idesc1, 0);
+      mma_commit_elect(bar + L::B_XEMPTY + s);
+      mma_commit_elect(bar + L::B_L1FULL);
+      if (it > 0) issue_l2(it - 1);
+    }
+    if (n_my > 0) issue_l2(n_my - 1);
+    __syncwarp();
   } else if (warp == WARP_MMA) {
     // ========================================================= MMA issuer
     // (pair: rank 0 issues M = 256 MMAs over both CTAs' SMEM and TMEM)
@@ -465,14 +542,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         TR(1, j);
         tc_fence_after();
         const uint32_t d = tbase + L::T_L2 + b * H2;
-        mma(d, onesd, w2bd, idesc2, 0);  // D = b2
+        if constexpr (PAIR) mma(d, onesd, w2bd, idesc2, 0);  // D = b2 (single CTA: + b2 in epilogue 2)
 #pragma unroll
         for (int kc = 0; kc < L::KC; ++kc)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = smem_desc(a20 + b * L::A2_BUF + kc * L::A2_CHUNK + k * 32, 1024, kSwizzle128);
             const uint64_t bd = smem_desc(w2 + kc * L::W2_CHUNK + k * 32, 1024, kSwizzle128);
-            mma(d, ad, bd, idesc2, 1);
+            mma(d, ad, bd, idesc2, PAIR || (kc | k) != 0);
           }
         commit(bar + L::B_A2EMPTY + b);
         commit(bar + L::B_L2FULL + b);
@@ -484,8 +561,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
         TR(0, it);
         tc_fence_after();
-        mma(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1
-        mma(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, 1);
+        if constexpr (PAIR) mma(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1 (single CTA: epilogue 1)
+        mma(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, PAIR ? 1 : 0);
         commit(bar + L::B_XEMPTY + s);
         commit(bar + L::B_L1FULL);
         if (it > 0) issue_l2(it - 1);
@@ -496,11 +573,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp >= WARP_EPI1) {
     const int half = (warp - WARP_EPI1) >> 2;
     if (a.act1 == SMLRT_RELU)
-      epilogue1<SMLRT_RELU, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane);
+      epilogue1<SMLRT_RELU, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane, a);
     else if (a.act1 == SMLRT_TANH)
-      epilogue1<SMLRT_TANH, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane);
+      epilogue1<SMLRT_TANH, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane, a);
     else
-      epilogue1<SMLRT_IDENTITY, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane);
+      epilogue1<SMLRT_IDENTITY, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane, a);
   } else {
     if (a.act2 == SMLRT_RELU)
       epilogue2<SMLRT_RELU, H1, H2, L, PAIR>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
@@ -688,6 +765,15 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
   }
   TcArgs a{};
   a.blob = reinterpret_cast<const uint8_t*>(m.tc_blob) + (pair ? pair_blob_off<H1, H2>() : 0);
+  {
+    const int F = m.in_features;
+    const float* b1 = m.host_params.data() + (size_t)H1 * F;
+    const float* b2 = b1 + H1 + (size_t)H2 * H1;
+    const float* w3 = b2 + H2;
+    std::memcpy(a.b1, b1, H1 * 4);
+    std::memcpy(a.b2, b2, H2 * 4);
+    std::memcpy(a.w3, w3, H2 * 4);
+  }
   a.F = m.in_features;
   a.act1 = m.layers[0].act;
   a.act2 = m.layers[1].act;
