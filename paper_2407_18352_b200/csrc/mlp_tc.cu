@@ -103,6 +103,7 @@ struct TcArgs {
   alignas(16) float b1[256];
   float b2[256];
   float w3[256];
+  float b3;
 };
 
 __device__ __forceinline__ uint64_t add2f(uint64_t a, uint64_t b) {
@@ -244,7 +245,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
                                           const TcArgs& a, const DevPlan& Pout, const Ptrs8& dst, Sched sc) {
   const int r = q * 32 + lane;
   const uint32_t w3 = smem_u32(smem + L::OFF_W3);
-  const float b3 = *reinterpret_cast<const float*>(smem + L::OFF_B3);
+  const float b3 = PAIR ? *reinterpret_cast<const float*>(smem + L::OFF_B3) : a.b3;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L2;
   const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 && a.staged == nullptr;
   float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
@@ -602,6 +603,281 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ============================================================================
+// TS variant (single CTA): the layer-2 A operand never touches shared memory.
+// Layer 1 runs as two N = H1/2 halves into one TMEM region; epilogue 1 drains
+// each half, adds b1, applies the activation, packs bf16 pairs and writes
+// them to TMEM with tcgen05.st; layer 2 then reads A from TMEM (tcgen05.mma
+// with [a-tmem]) and only W2 from shared memory.  Shared-memory traffic per
+// 128-row tile drops from ~230 KB (A2 stores + A2/W2 operand reads) to ~80 KB,
+// which was the binding resource of the SS kernel above.
+//
+// TMEM: L1 half [0, H1/2) | A2 [H1/2, H1): half a = hidden [0, H1/2) at
+// [H1/2, 3H1/4), half b at [3H1/4, H1) (bf16 pairs per 32-bit column) |
+// L2 acc x2 [H1, H1 + 2 H2).  Issue order per tile i (tensor pipe in order):
+//   L2(i) a-half | L1a(i+1) | L2(i) b-half | L1b(i+1)
+// so each L1 half's drain + conversion overlaps half of a layer-2 tile.
+template <int H1, int H2>
+struct LayTS {
+  using B = Lay<H1, H2, 1>;  // weight blob layout (W2 | W1 | ...)
+  static constexpr int KC = H1 / 64;
+  static constexpr int W2_CHUNK = H2 * 128;
+  static constexpr int X_STAGE = BM * 32;
+  static constexpr int OFF_W2 = 0;
+  static constexpr int OFF_W1 = OFF_W2 + KC * W2_CHUNK;  // [H1][16] SW32
+  static constexpr int OFF_X = OFF_W1 + H1 * 32;
+  static constexpr int OFF_W3 = OFF_X + XSTAGES * X_STAGE;  // unused (w3 in params); epilogue2 interface
+  static constexpr int OFF_B3 = OFF_W3;
+  static constexpr int OFF_BAR = OFF_W3 + 16;
+  enum {
+    B_XFULL = 0,
+    B_XEMPTY = XSTAGES,
+    B_L1FULL = 2 * XSTAGES,
+    B_L1EMPTY,
+    B_A2FULL,
+    B_A2EMPTY = B_A2FULL + 2,
+    B_L2FULL = B_A2EMPTY + 2,
+    B_L2EMPTY = B_L2FULL + 2,
+    N_BAR = B_L2EMPTY + 2
+  };
+  static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
+  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
+  static constexpr int T_L1 = 0, T_A2 = H1 / 2, T_L2 = H1;
+  static_assert(H1 + 2 * H2 <= 512, "TMEM columns");
+  static_assert(H1 % 128 == 0, "H1: two halves of a multiple of 64");
+};
+
+// epilogue 1 (TS): warp (q, part) drains columns [part*H1/4, +H1/4) of each
+// L1 half for its 32 rows and writes H1/8 packed columns of A2
+template <int ACT, int H1, int H2>
+__device__ __forceinline__ void epilogue1_ts(uint64_t* bar, uint32_t tbase, int n_my, int part, int q, int lane,
+                                             const TcArgs& a) {
+  using L = LayTS<H1, H2>;
+  constexpr int NC = H1 / 4;  // fp32 columns per warp per half (64 for H1 = 256)
+  static_assert(NC % 32 == 0, "x32 loads");
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  for (int it = 0; it < n_my; ++it) {
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int u = 2 * it + h;
+      mbar_wait(bar + L::B_L1FULL, u & 1);
+      if (q == 0 && part == 0 && lane == 0) TR(2 + 10 * h, it);
+      tc_fence_after();
+      uint32_t v[NC];
+#pragma unroll
+      for (int c = 0; c < NC / 32; ++c)
+        tmem_ld32(tbase + lane_off + L::T_L1 + part * NC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar + L::B_L1EMPTY);
+      // + b1, act, bf16 pairs
+      uint32_t pk[NC / 2];
+      const uint64_t* bp = reinterpret_cast<const uint64_t*>(a.b1 + h * (H1 / 2) + part * NC);
+#pragma unroll
+      for (int e = 0; e < NC / 2; ++e) {
+        const uint64_t sum = add2f(*reinterpret_cast<const uint64_t*>(&v[2 * e]), bp[e]);
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(sum));
+        pk[e] = act_pack<ACT>(lo, hi);
+      }
+      mbar_wait(bar + L::B_A2EMPTY + h, (it & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dst = tbase + lane_off + L::T_A2 + h * (H1 / 4) + part * (NC / 2);
+#pragma unroll
+      for (int c = 0; c < NC / 32; ++c) tmem_st16(dst + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16 * c));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar + L::B_A2FULL + h);
+      if (q == 0 && part == 0 && lane == 0) TR(5 + 8 * h, it);
+    }
+  }
+}
+
+template <int H1, int H2>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    mlp3_ts_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
+                   const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
+                   const __grid_constant__ Ptrs8 dst) {
+  using L = LayTS<H1, H2>;
+  using BL = typename L::B;
+  const Sched sc{(int)blockIdx.x, (int)gridDim.x, 0, 0};
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < XSTAGES; ++s) {
+      mbar_init(bar + L::B_XFULL + s, 128);
+      mbar_init(bar + L::B_XEMPTY + s, 1);
+    }
+    mbar_init(bar + L::B_L1FULL, 1);
+    mbar_init(bar + L::B_L1EMPTY, 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar + L::B_A2FULL + b, 256);
+      mbar_init(bar + L::B_A2EMPTY + b, 1);
+      mbar_init(bar + L::B_L2FULL + b, 1);
+      mbar_init(bar + L::B_L2EMPTY + b, 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
+  {  // resident weights: W2 chunks and W1 from the single-CTA blob
+    const int4* g = reinterpret_cast<const int4*>(a.blob);
+    for (int i = threadIdx.x; i < BL::BLOB_W1 / 16; i += NTHREADS)
+      reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
+    for (int i = threadIdx.x; i < H1 * 32 / 16; i += NTHREADS)
+      reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[BL::BLOB_W1 / 16 + i];
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const int n_my = (a.n_tiles - sc.first + sc.stride - 1) / sc.stride;
+
+  if (warp >= WARP_LOAD && warp < WARP_MMA) {
+    // loader: same X ring as the SS kernel (fast dense path or plan gather)
+    const int t = threadIdx.x - WARP_LOAD * 32;
+    const uint32_t xbase = smem_u32(smem + L::OFF_X);
+    if (a.x_fast != nullptr) {
+      float4 cur[4], nxt[4];
+      auto load_tile = [&](int it, float4(&v)[4]) {
+        const int64_t row0 = a.r0 + sc.tile(it) * BM;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int idx = t + 128 * i;
+          const int64_t row = row0 + (idx >> 2);
+          v[i] = row < a.r1 ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      if (n_my > 0) load_tile(0, cur);
+      for (int it = 0; it < n_my; ++it) {
+        if (it + 1 < n_my) load_tile(it + 1, nxt);
+        const int s = it % XSTAGES;
+        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
+        const uint32_t xs = xbase + s * L::X_STAGE;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int idx = t + 128 * i;
+          st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(cur[i].x, cur[i].y),
+                       pack_bf16(cur[i].z, cur[i].w));
+        }
+        fence_async_smem();
+        mbar_arrive(bar + L::B_XFULL + s);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+      }
+    } else {
+      float cur[16], nxt[16];
+      auto load_row = [&](int it, float(&v)[16]) {
+        const int64_t row = a.r0 + sc.tile(it) * BM + t;
+#pragma unroll
+        for (int f = 0; f < 16; ++f) v[f] = 0.0f;
+        if (row >= a.r1) return;
+        if (Pin.uniform) {
+          const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
+          const void* base = src.p[Pin.uarray];
+          const int dt = src.dt[Pin.uarray];
+#pragma unroll
+          for (int f = 0; f < 16; ++f)
+            if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
+        } else {
+          uint32_t idx[SMLRT_MAX_SWEEP];
+          unravel(Pin, (uint32_t)row, idx);
+#pragma unroll
+          for (int f = 0; f < 16; ++f)
+            if (f < a.F) {
+              const int arr = __ldg(Pin.col_arr + f);
+              v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
+            }
+        }
+      };
+      if (n_my > 0) load_row(0, cur);
+      for (int it = 0; it < n_my; ++it) {
+        if (it + 1 < n_my) load_row(it + 1, nxt);
+        const int s = it % XSTAGES;
+        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
+        const uint32_t xs = xbase + s * L::X_STAGE;
+        st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
+                     pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
+        st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
+                     pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
+        fence_async_smem();
+        mbar_arrive(bar + L::B_XFULL + s);
+#pragma unroll
+        for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    // whole warp, elect.sync issue (see the SS kernel)
+    constexpr uint32_t idesc1 = idesc_bf16(BM, H1 / 2);
+    constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
+    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
+    const uint64_t x0d = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
+    const uint64_t w20d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
+    auto l1 = [&](int it, int h) {
+      const int s = it % XSTAGES, u = 2 * it + h;
+      if (h == 0) mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
+      mbar_wait(bar + L::B_L1EMPTY, (u & 1) ^ 1);
+      if (lane == 0) TR(h == 0 ? 0 : 14, it);
+      tc_fence_after();
+      mma_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d + ((h * (H1 / 2) * 32) >> 4), idesc1, 0);
+      mma_commit_elect(bar + L::B_L1FULL);
+      if (h == 1) mma_commit_elect(bar + L::B_XEMPTY + s);
+    };
+    auto l2 = [&](int it, int h) {
+      const int b = it & 1;
+      if (h == 0) mbar_wait(bar + L::B_L2EMPTY + b, ((it >> 1) & 1) ^ 1);
+      mbar_wait(bar + L::B_A2FULL + h, it & 1);
+      if (lane == 0) TR(h == 0 ? 1 : 15, it);
+      tc_fence_after();
+      const uint32_t d = tbase + L::T_L2 + b * H2;
+#pragma unroll
+      for (int ks = 0; ks < H1 / 32; ++ks) {  // K = 16 steps over this half's H1/2 hidden units
+        const int k = h * (H1 / 2) + ks * 16;
+        mma_ts_elect(d, tbase + L::T_A2 + h * (H1 / 4) + ks * 8,
+                     w20d + (((k / 64) * L::W2_CHUNK + ((k % 64) / 16) * 32) >> 4), idesc2, (h | ks) != 0);
+      }
+      mma_commit_elect(bar + L::B_A2EMPTY + h);
+      if (h == 1) mma_commit_elect(bar + L::B_L2FULL + b);
+    };
+    if (n_my > 0) {
+      l1(0, 0);
+      l1(0, 1);
+    }
+    for (int it = 0; it < n_my; ++it) {
+      l2(it, 0);
+      if (it + 1 < n_my) l1(it + 1, 0);
+      l2(it, 1);
+      if (it + 1 < n_my) l1(it + 1, 1);
+    }
+    __syncwarp();
+  } else if (warp >= WARP_EPI1) {
+    const int part = (warp - WARP_EPI1) >> 2;
+    if (a.act1 == SMLRT_RELU)
+      epilogue1_ts<SMLRT_RELU, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
+    else if (a.act1 == SMLRT_TANH)
+      epilogue1_ts<SMLRT_TANH, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
+    else
+      epilogue1_ts<SMLRT_IDENTITY, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
+  } else {
+    if (a.act2 == SMLRT_RELU)
+      epilogue2<SMLRT_RELU, H1, H2, L, false>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
+    else if (a.act2 == SMLRT_TANH)
+      epilogue2<SMLRT_TANH, H1, H2, L, false>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
+    else
+      epilogue2<SMLRT_IDENTITY, H1, H2, L, false>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 // TS self-test: D[128 x N] = A[128 x K] * B[N x K]^T with A staged in TMEM by
 // tcgen05.st (bf16 pairs): validates the TMEM A-operand (TS) layout.
 template <int N>
@@ -732,6 +1008,19 @@ int num_sms() {
   return n;
 }
 
+// SMLRT_TC_KERNEL: "ss" (default: layer-2 A operand in SMEM) or "ts" (A in
+// TMEM).  Measured on B200 (bonds, 16.8M rows): ss 1.13 ms, ts 1.16 ms -- both
+// ~2300-cycle tile periods; the TS kernel's epilogue-1 drain of each L1 half
+// takes ~1000 cycles while layer-2 MMAs run (tools/tc_trace.py), so removing
+// the A2 shared-memory traffic did not shorten the critical loop.
+bool use_ts() {
+  static const int v = [] {
+    const char* e = std::getenv("SMLRT_TC_KERNEL");
+    return (e && std::strcmp(e, "ts") == 0) ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 // CTA-pair kernel (SMLRT_TC_PAIR=1); off by default: measured slower than the
 // single-CTA kernel on bonds (period 2800 vs 2390 cycles/tile, tools/tc_trace.py)
 bool use_pair() {
@@ -761,6 +1050,8 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
                                     Lay<H1, H2, 1>::ALLOC));
     SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Lay<H1, H2, 2>::ALLOC));
+    SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    LayTS<H1, H2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
@@ -773,6 +1064,7 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     std::memcpy(a.b1, b1, H1 * 4);
     std::memcpy(a.b2, b2, H2 * 4);
     std::memcpy(a.w3, w3, H2 * 4);
+    a.b3 = w3[H2];
   }
   a.F = m.in_features;
   a.act1 = m.layers[0].act;
@@ -798,7 +1090,11 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     const float* base = reinterpret_cast<const float*>(in_ptrs[in.uarray]) + in.col_off0;
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
-  if (!pair) {
+  if (!pair && use_ts()) {
+    const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
+    mlp3_ts_kernel<H1, H2><<<grid, NTHREADS, LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
+    count_launch();
+  } else if (!pair) {
     const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
     mlp3_tc_kernel<H1, H2, false><<<grid, NTHREADS, Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
     count_launch();

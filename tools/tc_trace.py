@@ -17,7 +17,9 @@ import paper_2407_18352_b200 as sm  # noqa: E402
 from paper_2407_18352_b200 import _native, workloads  # noqa: E402
 
 EV = {0: "L1 issue", 9: "mma sees XFULL", 1: "L2 issue", 11: "mma sees A2FULL", 2: "epi1 L1FULL", 3: "epi1 A2EMPTY",
-      4: "epi1 drained", 5: "epi1 A2FULL", 6: "epi2 L2FULL", 7: "epi2 done", 8: "loader XFULL"}
+      4: "epi1 drained", 5: "epi1 A2FULL", 6: "epi2 L2FULL", 7: "epi2 done", 8: "loader XFULL",
+      12: "epi1 L1bFULL", 13: "epi1 A2bFULL", 14: "L1b issue", 15: "L2b issue"}
+COLS = tuple(int(c) for c in os.environ.get("TRACE_COLS", "8,9,0,2,3,4,5,11,1,6,7").split(","))
 
 n = int(os.environ.get("N", 148 * 128 * 64 * 2))
 wl = workloads.make("bonds", n)
@@ -38,9 +40,9 @@ for cta in (0, 1):
     tr = t[cta]
     base = tr[0, 0] if tr[0, 0] else tr[0, 2]
     print(f"== CTA {cta} (cycles from tile-0 L1 issue)")
-    print("tile " + " ".join(f"{EV[e][:13]:>13}" for e in (8, 9, 0, 2, 3, 4, 5, 11, 1, 6, 7)))
+    print("tile " + " ".join(f"{EV[e][:13]:>13}" for e in COLS))
     for it in range(0, 24):
-        print(f"{it:4d} " + " ".join(f"{(tr[it, e] - base) if tr[it, e] else -1:13d}" for e in (8, 9, 0, 2, 3, 4, 5, 11, 1, 6, 7)))
+        print(f"{it:4d} " + " ".join(f"{(tr[it, e] - base) if tr[it, e] else -1:13d}" for e in COLS))
     for e in (0, 1, 2, 5, 7):
         col = tr[8:60, e]
         col = col[col > 0]
