@@ -35,8 +35,13 @@ using namespace ptx;
 constexpr int BM = 128;
 constexpr int KX = 16;
 constexpr int XSTAGES = 2;
-constexpr int WARP_EPI2 = 0, WARP_EPI1 = 4, WARP_LOAD = 12, WARP_MMA = 16;
-constexpr int NTHREADS = 17 * 32;
+#ifndef SMLRT_EPI1_PARTS
+#define SMLRT_EPI1_PARTS 2
+#endif
+// epilogue-1 warps per TMEM lane quarter: each drains H1/NP columns
+constexpr int NP = SMLRT_EPI1_PARTS;
+constexpr int WARP_EPI2 = 0, WARP_EPI1 = 4, WARP_LOAD = 4 + 4 * NP, WARP_MMA = WARP_LOAD + 4;
+constexpr int NTHREADS = (WARP_MMA + 1) * 32;
 
 // Biases ride on the tensor cores: a constant "ones" tile [128 x 16] (columns
 // 0 and 1 = 1.0) times a bias tile [N x 16] holding bf16(b) in k=0 and
@@ -183,7 +188,7 @@ __device__ __forceinline__ void arrive_mma(uint64_t* bar) {
 template <int ACT, int H1, int H2, class L, bool PAIR>
 __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int half,
                                           int q, int lane, const TcArgs& a) {
-  constexpr int HC = H1 / 2;
+  constexpr int HC = H1 / NP;  // columns this warp drains (`half` = part index)
   const int r = q * 32 + lane;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L1 + half * HC;
   // swizzled 16-B chunk j of row r lives at rowbase + ((j ^ (r&7)) << 4)
@@ -341,9 +346,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(bar + L::B_XEMPTY + s, 1);
     }
     mbar_init(bar + L::B_L1FULL, 1);
-    mbar_init(bar + L::B_L1EMPTY, 256 * NS);
+    mbar_init(bar + L::B_L1EMPTY, 128 * NP * NS);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar + L::B_A2FULL + b, 256 * NS);
+      mbar_init(bar + L::B_A2FULL + b, 128 * NP * NS);
       mbar_init(bar + L::B_A2EMPTY + b, 1);
       mbar_init(bar + L::B_L2FULL + b, 1);
       mbar_init(bar + L::B_L2EMPTY + b, 128 * NS);
@@ -572,7 +577,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp >= WARP_EPI1) {
-    const int half = (warp - WARP_EPI1) >> 2;
+    const int half = (warp - WARP_EPI1) >> 2;  // part index in [0, NP)
     if (a.act1 == SMLRT_RELU)
       epilogue1<SMLRT_RELU, H1, H2, L, PAIR>(smem, bar, tbase, n_my, half, warp & 3, lane, a);
     else if (a.act1 == SMLRT_TANH)
@@ -653,7 +658,7 @@ template <int ACT, int H1, int H2>
 __device__ __forceinline__ void epilogue1_ts(uint64_t* bar, uint32_t tbase, int n_my, int part, int q, int lane,
                                              const TcArgs& a) {
   using L = LayTS<H1, H2>;
-  constexpr int NC = H1 / 4;  // fp32 columns per warp per half (64 for H1 = 256)
+  constexpr int NC = H1 / 2 / NP;  // fp32 columns per warp per half (64 for H1 = 256, NP = 2)
   static_assert(NC % 32 == 0, "x32 loads");
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
   for (int it = 0; it < n_my; ++it) {
@@ -712,9 +717,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(bar + L::B_XEMPTY + s, 1);
     }
     mbar_init(bar + L::B_L1FULL, 1);
-    mbar_init(bar + L::B_L1EMPTY, 256);
+    mbar_init(bar + L::B_L1EMPTY, 128 * NP);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar + L::B_A2FULL + b, 256);
+      mbar_init(bar + L::B_A2FULL + b, 128 * NP);
       mbar_init(bar + L::B_A2EMPTY + b, 1);
       mbar_init(bar + L::B_L2FULL + b, 1);
       mbar_init(bar + L::B_L2EMPTY + b, 128);
@@ -1031,6 +1036,12 @@ bool use_pair() {
   return v != 0;
 }
 
+// TS epilogue drains x32 column groups per warp
+template <int H1>
+constexpr bool ts_ok() {
+  return (H1 / 2 / NP) % 32 == 0;
+}
+
 template <int H1, int H2>
 constexpr size_t pair_blob_off() {
   return ((size_t)Lay<H1, H2, 1>::BLOB + 1023) & ~size_t(1023);
@@ -1050,8 +1061,9 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
                                     Lay<H1, H2, 1>::ALLOC));
     SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Lay<H1, H2, 2>::ALLOC));
-    SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    LayTS<H1, H2>::ALLOC));
+    if constexpr (ts_ok<H1>())
+      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      LayTS<H1, H2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
@@ -1090,10 +1102,12 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     const float* base = reinterpret_cast<const float*>(in_ptrs[in.uarray]) + in.col_off0;
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
-  if (!pair && use_ts()) {
-    const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-    mlp3_ts_kernel<H1, H2><<<grid, NTHREADS, LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
-    count_launch();
+  if (!pair && use_ts() && ts_ok<H1>()) {
+    if constexpr (ts_ok<H1>()) {
+      const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
+      mlp3_ts_kernel<H1, H2><<<grid, NTHREADS, LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
+      count_launch();
+    }
   } else if (!pair) {
     const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
     mlp3_tc_kernel<H1, H2, false><<<grid, NTHREADS, Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
