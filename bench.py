@@ -271,8 +271,10 @@ def run_ours(args, rank, world, local):
     traffic = None
     if tj.exists():
         t = json.loads(tj.read_text()).get(spec.name)
-        traffic = t and t["dram_bytes_per_launch"]
-    roof.update({"traffic": traffic, "traffic_unit": "DRAM bytes/launch (ncu, profiles/traffic.json)",
+        traffic = t and t.get("dram_bytes_per_region")
+        if traffic and wl.elements != spec.elements:
+            traffic = traffic * wl.elements / spec.elements
+    roof.update({"traffic": traffic, "traffic_unit": "DRAM read+write bytes per region call (ncu --set full, profiles/traffic.json)",
                  "alg_bytes_per_launch": wl.elements * spec.bytes_per_elem, "kernel_ms": round(k_ms, 4), "hbm_frac": round(f_hbm, 4),
                  "compute_frac": round(f_cmp, 4), "flops_per_elem": spec.flops_per_elem,
                  "bytes_per_elem": spec.bytes_per_elem})
