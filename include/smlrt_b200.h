@@ -58,6 +58,10 @@ typedef enum { SMLRT_FP32_EXACT = 0, SMLRT_BF16 = 1 } smlrt_precision_t;
 #define SMLRT_COMMIT_FUSED 0x0   /* epilogue writes outputs directly          */
 #define SMLRT_COMMIT_CHECKED 0x1 /* stage, check finiteness, then write       */
 #define SMLRT_FORCE_UNFUSED 0x2  /* gather -> per-layer -> scatter (diagnostic)*/
+#define SMLRT_SYNC_STATUS 0x4    /* reset *d_status first; afterwards copy it   */
+                                 /* to host, synchronise the stream and return */
+                                 /* SMLRT_E_NONFINITE if it is set (one call,  */
+                                 /* one sync: runtime.py:341's raise)           */
 
 /*
  * One RHS view of a tensor functor applied to one array: the flattening of

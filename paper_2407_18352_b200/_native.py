@@ -21,7 +21,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsmlrt_b200.so"
 
 TO, FROM = 0, 1
 FP32_EXACT, BF16 = 0, 1
-COMMIT_FUSED, COMMIT_CHECKED, FORCE_UNFUSED = 0, 1, 2
+COMMIT_FUSED, COMMIT_CHECKED, FORCE_UNFUSED, SYNC_STATUS = 0, 1, 2, 4
 ACT = {"identity": 0, "relu": 1, "tanh": 2}
 
 

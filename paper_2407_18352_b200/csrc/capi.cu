@@ -256,6 +256,10 @@ extern "C" int smlrt_region_workspace(smlrt_plan_t in, smlrt_plan_t out, smlrt_m
   return SMLRT_OK;
 }
 
+static int region_launch(smlrt_plan_t pin, const void* const* in_ptrs, const int32_t* in_dt, smlrt_plan_t pout,
+                         void* const* out_ptrs, const int32_t* out_dt, smlrt_model_t m, int64_t r0, int64_t r1,
+                         int32_t flags, void* workspace, cudaStream_t s, uint32_t* status);
+
 extern "C" int smlrt_region_infer(smlrt_plan_t pin, const void* const* in_ptrs, const int32_t* in_dt,
                                   smlrt_plan_t pout, void* const* out_ptrs, const int32_t* out_dt,
                                   smlrt_model_t m, int64_t r0, int64_t r1, int32_t flags,
@@ -280,6 +284,24 @@ extern "C" int smlrt_region_infer(smlrt_plan_t pin, const void* const* in_ptrs, 
   SMLRT_CUDA(cudaGetDevice(&dev));
   if (dev != m->device) return fail(SMLRT_E_INVALID, "region_infer: model lives on another device");
   cudaStream_t s = (cudaStream_t)stream;
+  if (flags & SMLRT_SYNC_STATUS) {
+    SMLRT_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
+    const int rc = region_launch(pin, in_ptrs, in_dt, pout, out_ptrs, out_dt, m, r0, r1, flags, workspace, s, status);
+    if (rc) return rc;
+    static thread_local uint32_t* h_status = nullptr;  // pinned, one per host thread
+    if (!h_status) SMLRT_CUDA(cudaMallocHost(&h_status, sizeof(uint32_t)));
+    SMLRT_CUDA(cudaMemcpyAsync(h_status, status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SMLRT_CUDA(cudaStreamSynchronize(s));
+    if (*h_status & SMLRT_STATUS_NONFINITE) return fail(SMLRT_E_NONFINITE, "forward pass produced NaN/inf");
+    return SMLRT_OK;
+  }
+  return region_launch(pin, in_ptrs, in_dt, pout, out_ptrs, out_dt, m, r0, r1, flags, workspace, s, status);
+}
+
+// the launches of smlrt_region_infer (validated arguments)
+static int region_launch(smlrt_plan_t pin, const void* const* in_ptrs, const int32_t* in_dt, smlrt_plan_t pout,
+                         void* const* out_ptrs, const int32_t* out_dt, smlrt_model_t m, int64_t r0, int64_t r1,
+                         int32_t flags, void* workspace, cudaStream_t s, uint32_t* status) {
   DevPlan din, dout;
   if (int rc = device_tables(pin, &din, in_dt, pin->n_arrays)) return rc;
   if (int rc = device_tables(pout, &dout, out_dt, pout->n_arrays)) return rc;

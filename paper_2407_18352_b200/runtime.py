@@ -460,21 +460,33 @@ class Runtime:
         map_to = _ns_since(t0)
 
         t0 = time.perf_counter_ns()
-        status.zero_()
         iptr, idt = pin.ptrs_and_dtypes()
         optr, odt = pout.ptrs_and_dtypes()
         flags = _native.COMMIT_CHECKED if self.commit == "checked" else _native.COMMIT_FUSED
+        # device-resident outputs: status reset, launch, status read-back and
+        # the stream sync happen inside one native call (SMLRT_SYNC_STATUS)
+        # (kernel timing wants the events around the launches alone: old path)
+        sync_native = not self.time_kernels and all(m.array.is_device for m in host_out)
+        if sync_native:
+            flags |= _native.SYNC_STATUS
+        else:
+            status.zero_()
         if self.time_kernels:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(stream)
-        _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1,
-                             flags, None, stream.cuda_stream, status.data_ptr())
+        bad = 0
+        try:
+            _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1,
+                                 flags, None, stream.cuda_stream, status.data_ptr())
+        except NonFiniteOutputError:
+            bad = 1
         if self.time_kernels:
             ev[1].record(stream)
             self.kernel_events.append(ev)
-        for m, d in zip(host_out, out_maps):
-            self._staging.download(m.array, d.array)
-        bad = int(status.item())  # synchronises the stream
+        if not sync_native:
+            for m, d in zip(host_out, out_maps):
+                self._staging.download(m.array, d.array)
+            bad = int(status.item())  # synchronises the stream
         infer_ns = _ns_since(t0)
 
         t0 = time.perf_counter_ns()
