@@ -42,6 +42,10 @@ constexpr int XSTAGES = 2;
 constexpr int NP = SMLRT_EPI1_PARTS;
 constexpr int WARP_EPI2 = 0, WARP_EPI1 = 4, WARP_LOAD = 4 + 4 * NP, WARP_MMA = WARP_LOAD + 4;
 constexpr int NTHREADS = (WARP_MMA + 1) * 32;
+#ifndef SMLRT_LDEPTH
+#define SMLRT_LDEPTH 2
+#endif
+constexpr int LDEPTH = SMLRT_LDEPTH;  // X tiles of global loads in flight per loader thread
 
 // Biases ride on the tensor cores: a constant "ones" tile [128 x 16] (columns
 // 0 and 1 = 1.0) times a bias tile [N x 16] holding bf16(b) in k=0 and
@@ -79,7 +83,9 @@ struct Lay {
     B_A2EMPTY = B_A2FULL + 2,
     B_L2FULL = B_A2EMPTY + 2,
     B_L2EMPTY = B_L2FULL + 2,
-    N_BAR = B_L2EMPTY + 2
+    B_L1FULL2 = B_L2EMPTY + 2,  // single-CTA kernel: layer 1 as two N = H1/2 halves
+    B_L1EMPTY2,
+    N_BAR
   };
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
   static constexpr int BYTES = OFF_TMEM + 16;
@@ -230,6 +236,9 @@ __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t
         f = fb;
       }
       const uint32_t coff = boff + (c >> 2) * L::A2_CHUNK;
+#if defined(SMLRT_ABLATE) && SMLRT_ABLATE == 1  // timing experiment only: no A2 stores
+      if (f[0] == 12345.0f)
+#endif
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         st_shared_v4(xo[((c >> 1) & 1) * 4 + (c & 1) * 2 + j] + coff, act_pack<ACT>(f[8 * j], f[8 * j + 1]),
@@ -240,6 +249,75 @@ __device__ __forceinline__ void epilogue1(uint8_t* smem, uint64_t* bar, uint32_t
     arrive_mma<PAIR>(bar + L::B_A2FULL + b);
     if (q == 0 && half == 0 && lane == 0) TR(5, it);
   }
+}
+
+// Single-CTA epilogue 1 over layer 1 split in two N = H1/2 halves, each with
+// its own TMEM columns and full/empty barriers: the MMA warp issues half a of
+// tile i+1 as soon as half a of tile i is drained, so the drain of one half
+// overlaps the layer-1 MMA (and its commit latency) of the other instead of
+// serialising behind a single-buffered accumulator.  Warp (q, part) drains
+// columns [part*H1/4, +H1/4) of each half for its 32 rows.
+template <int ACT, int H1, int H2, class L, int PART>
+__device__ __forceinline__ void epilogue1_split(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int q,
+                                                int lane, const TcArgs& a) {
+  static_assert(NP == 2, "two epilogue-1 warps per lane quarter");
+  constexpr int HH = H1 / 2, HC = HH / 2;
+  static_assert(HC % 16 == 0 && HC <= 64, "x16 loads, <= 64 registers per half");
+  const int r = q * 32 + lane;
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  const uint32_t a2row = smem_u32(smem + L::OFF_A2) + r * 128;
+  for (int it = 0; it < n_my; ++it) {
+    const int b = it & 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mbar_wait(bar + (h == 0 ? L::B_L1FULL : L::B_L1FULL2), it & 1);
+      if (q == 0 && PART == 0 && lane == 0) TR(h == 0 ? 2 : 12, it);
+      tc_fence_after();
+      const int col0 = h * HH + PART * HC;  // first hidden unit of this warp's columns (compile-time)
+      // drain the whole half into registers first and release its TMEM
+      // columns at once; only then wait for the A2 buffer (which frees when
+      // layer 2 of tile it-2 completes)
+      uint32_t v[HC];
+#pragma unroll
+      for (int c = 0; c < HC / 16; ++c)
+        tmem_ld16(tbase + lane_off + L::T_L1 + col0 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar + (h == 0 ? L::B_L1EMPTY : L::B_L1EMPTY2));
+      if (h == 0) mbar_wait(bar + L::B_A2EMPTY + b, ((it >> 1) & 1) ^ 1);
+#pragma unroll
+      for (int c = 0; c < HC / 16; ++c) {
+        const int col = col0 + c * 16;
+        float f[16];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint64_t bb = *reinterpret_cast<const uint64_t*>(a.b1 + col + 2 * e);  // uniform LDCU
+          const uint64_t sum = add2f(*reinterpret_cast<const uint64_t*>(&v[16 * c + 2 * e]), bb);
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(f[2 * e]), "=f"(f[2 * e + 1]) : "l"(sum));
+        }
+        // SW128 K-major: hidden unit `col` -> chunk col/64, 16-B slot (col%64)/8 ^ (r&7)
+        const uint32_t base = a2row + b * L::A2_BUF + (col >> 6) * L::A2_CHUNK;
+        const int j0 = (col & 63) >> 3;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          st_shared_v4(base + (((j0 + j) ^ (r & 7)) << 4), act_pack<ACT>(f[8 * j], f[8 * j + 1]),
+                       act_pack<ACT>(f[8 * j + 2], f[8 * j + 3]), act_pack<ACT>(f[8 * j + 4], f[8 * j + 5]),
+                       act_pack<ACT>(f[8 * j + 6], f[8 * j + 7]));
+      }
+    }
+    fence_async_smem();
+    mbar_arrive(bar + L::B_A2FULL + b);
+    if (q == 0 && PART == 0 && lane == 0) TR(5, it);
+  }
+}
+
+template <int ACT, int H1, int H2, class L>
+__device__ __forceinline__ void epilogue1_split_dispatch(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my,
+                                                         int part, int q, int lane, const TcArgs& a) {
+  if (part == 0)
+    epilogue1_split<ACT, H1, H2, L, 0>(smem, bar, tbase, n_my, q, lane, a);
+  else
+    epilogue1_split<ACT, H1, H2, L, 1>(smem, bar, tbase, n_my, q, lane, a);
 }
 
 // ------------------------------------------------------------ epilogue 2
@@ -347,6 +425,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     mbar_init(bar + L::B_L1FULL, 1);
     mbar_init(bar + L::B_L1EMPTY, 128 * NP * NS);
+    mbar_init(bar + L::B_L1FULL2, 1);
+    mbar_init(bar + L::B_L1EMPTY2, 128 * NP * NS);
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar + L::B_A2FULL + b, 128 * NP * NS);
       mbar_init(bar + L::B_A2EMPTY + b, 1);
@@ -391,35 +471,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int t = threadIdx.x - WARP_LOAD * 32;
     const uint32_t xbase = smem_u32(smem + L::OFF_X);
     if (a.x_fast != nullptr) {
-      // tile = 2048 contiguous floats: thread t moves float4 #(t + 128 i), i < 4
-      float4 cur[4], nxt[4];
+      // tile = 2048 contiguous floats: thread t moves float4 #(t + 128 i), i < 4.
+      // Loads run LDEPTH tiles ahead in registers: with one tile in flight the
+      // loader had 8 KB outstanding per SM, ~0.9 TB/s at HBM latency, which
+      // capped the whole kernel (the MMA warp waited on X tiles).
+      float4 buf[LDEPTH][4];
       auto load_tile = [&](int it, float4(&v)[4]) {
         const int64_t row0 = a.r0 + sc.tile(it) * BM;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int idx = t + 128 * i;
           const int64_t row = row0 + (idx >> 2);
-          v[i] = row < a.r1 ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[i] = (it < n_my && row < a.r1)
+                     ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       };
-      if (n_my > 0) load_tile(0, cur);
-      for (int it = 0; it < n_my; ++it) {
-        if (it + 1 < n_my) load_tile(it + 1, nxt);
-        const int s = it % XSTAGES;
-        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-        const uint32_t xs = xbase + s * L::X_STAGE;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = t + 128 * i;
-          st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(cur[i].x, cur[i].y),
-                       pack_bf16(cur[i].z, cur[i].w));
+      for (int d = 0; d < LDEPTH; ++d) load_tile(d, buf[d]);
+      for (int it0 = 0; it0 < n_my; it0 += LDEPTH) {
+#pragma unroll
+        for (int d = 0; d < LDEPTH; ++d) {
+          const int it = it0 + d;
+          if (it >= n_my) break;
+          const int s = it % XSTAGES;
+          mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
+          const uint32_t xs = xbase + s * L::X_STAGE;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int idx = t + 128 * i;
+            st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(buf[d][i].x, buf[d][i].y),
+                         pack_bf16(buf[d][i].z, buf[d][i].w));
+          }
+          fence_async_smem();
+          arrive_mma<PAIR>(bar + L::B_XFULL + s);
+          if (t == 0) TR(8, it);
+          load_tile(it + LDEPTH, buf[d]);
         }
-        fence_async_smem();
-        arrive_mma<PAIR>(bar + L::B_XFULL + s);
-        if (t == 0) TR(8, it);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       }
     } else {
       // general plan-driven gather: thread = tile row
@@ -486,27 +574,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_after();
       const uint32_t d = tbase + L::T_L2 + b * H2;
       const uint64_t ab = a20d + ((b * L::A2_BUF) >> 4);
+#if defined(SMLRT_ABLATE) && SMLRT_ABLATE == 2  // timing experiment only: one L2 MMA per tile
+      mma_ss_elect(d, ab, w20d, idesc2, 0);
+#else
 #pragma unroll
       for (int kc = 0; kc < L::KC; ++kc)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           mma_ss_elect(d, ab + ((kc * L::A2_CHUNK + k * 32) >> 4), w20d + ((kc * L::W2_CHUNK + k * 32) >> 4), idesc2,
                        (kc | k) != 0);
+#endif
       mma_commit_elect(bar + L::B_A2EMPTY + b);
       mma_commit_elect(bar + L::B_L2FULL + b);
     };
+    constexpr uint32_t idesc1h = idesc_bf16(BM, H1 / 2);
     for (int it = 0; it < n_my; ++it) {
       const int s = it % XSTAGES;
       mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
       if (lane == 0) TR(9, it);
-      mbar_wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
-      if (lane == 0) TR(0, it);
-      tc_fence_after();
-      mma_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d, idesc1, 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // layer 1 in two halves with separate TMEM columns / barriers
+        mbar_wait(bar + (h == 0 ? L::B_L1EMPTY : L::B_L1EMPTY2), (it & 1) ^ 1);
+        if (lane == 0 && h == 0) TR(0, it);
+        tc_fence_after();
+        mma_ss_elect(tbase + L::T_L1 + h * (H1 / 2), x0d + ((s * L::X_STAGE) >> 4),
+                     w1d + ((h * (H1 / 2) * 32) >> 4), idesc1h, 0);
+        mma_commit_elect(bar + (h == 0 ? L::B_L1FULL : L::B_L1FULL2));
+      }
       mma_commit_elect(bar + L::B_XEMPTY + s);
-      mma_commit_elect(bar + L::B_L1FULL);
       if (it > 0) issue_l2(it - 1);
     }
+    (void)idesc1;
     if (n_my > 0) issue_l2(n_my - 1);
     __syncwarp();
   } else if (warp == WARP_MMA) {
@@ -576,6 +674,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (n_my > 0) issue_l2(n_my - 1);
     }
     __syncwarp();
+  } else if (warp >= WARP_EPI1 && !PAIR) {
+    const int part = (warp - WARP_EPI1) >> 2;
+    if (a.act1 == SMLRT_RELU)
+      epilogue1_split_dispatch<SMLRT_RELU, H1, H2, L>(smem, bar, tbase, n_my, part, warp & 3, lane, a);
+    else if (a.act1 == SMLRT_TANH)
+      epilogue1_split_dispatch<SMLRT_TANH, H1, H2, L>(smem, bar, tbase, n_my, part, warp & 3, lane, a);
+    else
+      epilogue1_split_dispatch<SMLRT_IDENTITY, H1, H2, L>(smem, bar, tbase, n_my, part, warp & 3, lane, a);
   } else if (warp >= WARP_EPI1) {
     const int half = (warp - WARP_EPI1) >> 2;  // part index in [0, NP)
     if (a.act1 == SMLRT_RELU)
@@ -746,33 +852,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int t = threadIdx.x - WARP_LOAD * 32;
     const uint32_t xbase = smem_u32(smem + L::OFF_X);
     if (a.x_fast != nullptr) {
-      float4 cur[4], nxt[4];
+      float4 buf[LDEPTH][4];  // LDEPTH tiles of loads in flight (see the SS kernel)
       auto load_tile = [&](int it, float4(&v)[4]) {
         const int64_t row0 = a.r0 + sc.tile(it) * BM;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int idx = t + 128 * i;
           const int64_t row = row0 + (idx >> 2);
-          v[i] = row < a.r1 ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[i] = (it < n_my && row < a.r1)
+                     ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       };
-      if (n_my > 0) load_tile(0, cur);
-      for (int it = 0; it < n_my; ++it) {
-        if (it + 1 < n_my) load_tile(it + 1, nxt);
-        const int s = it % XSTAGES;
-        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-        const uint32_t xs = xbase + s * L::X_STAGE;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = t + 128 * i;
-          st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(cur[i].x, cur[i].y),
-                       pack_bf16(cur[i].z, cur[i].w));
+      for (int d = 0; d < LDEPTH; ++d) load_tile(d, buf[d]);
+      for (int it0 = 0; it0 < n_my; it0 += LDEPTH) {
+#pragma unroll
+        for (int d = 0; d < LDEPTH; ++d) {
+          const int it = it0 + d;
+          if (it >= n_my) break;
+          const int s = it % XSTAGES;
+          mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
+          const uint32_t xs = xbase + s * L::X_STAGE;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int idx = t + 128 * i;
+            st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(buf[d][i].x, buf[d][i].y),
+                         pack_bf16(buf[d][i].z, buf[d][i].w));
+          }
+          fence_async_smem();
+          mbar_arrive(bar + L::B_XFULL + s);
+          load_tile(it + LDEPTH, buf[d]);
         }
-        fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       }
     } else {
       float cur[16], nxt[16];
