@@ -34,7 +34,10 @@ using namespace ptx;
 
 constexpr int BM = 128;
 constexpr int KX = 16;
-constexpr int XSTAGES = 2;
+#ifndef SMLRT_XSTAGES
+#define SMLRT_XSTAGES 2
+#endif
+constexpr int XSTAGES = SMLRT_XSTAGES;
 #ifndef SMLRT_EPI1_PARTS
 #define SMLRT_EPI1_PARTS 2
 #endif
