@@ -223,3 +223,23 @@ def test_stats_bounded_by_wall(cuda, jdir):
         wall = time.perf_counter_ns() - t0
         st = rt.stats(h)
     assert st.map_to_ns + st.map_from_ns + st.infer_ns <= wall and st.invocations == 5
+
+
+def test_status_word_resets_between_calls(cuda, tmp_path, jdir):
+    """The status word is reset per call on both native paths (one-call sync
+    and the event-timed asynchronous path): a NonFinite call does not poison
+    the next one, and both paths raise it."""
+    sm.save_model(sm.Model(5, 1, [sm.DenseLayer(np.full((1, 5), 1e38, np.float32), np.zeros(1, np.float32),
+                                                "identity")]), tmp_path / "big")
+    bad, t, _, _ = make_region("infer", model=str(tmp_path / "big"), name="bad")
+    t.view().fill_(10.0)
+    good, _, _, _ = make_region("infer", model=jdir, name="good")
+    for timed in (False, True):
+        with sm.Runtime() as rt:
+            rt.time_kernels = timed
+            hb, hg = rt.register_region(bad), rt.register_region(good)
+            with pytest.raises(NonFiniteOutputError):
+                rt.invoke_region(hb)
+            assert rt.invoke_region(hg).path_taken == "surrogate"
+            with pytest.raises(NonFiniteOutputError):
+                rt.invoke_region(hb)

@@ -66,3 +66,24 @@ def test_minibude_full_size_subsample(cuda, tmp_path):
     x = np.ascontiguousarray(wl.arrays["poses"][:, idx].T)
     ref, _ = c_oracle.mlp_f32(wl.layers, x)
     check_tol(got[idx], ref[:, 0].astype(np.float64))
+
+
+def test_minibude_tcgen05_layer1_variant(cuda, tmp_path):
+    """The opt-in tcgen05 layer-1 kernel (SMLRT_WIDE_L1=tc) meets the same
+    tolerances (run in a subprocess: the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "import test_gpu_wide as t, pathlib, tempfile;"
+            "from paper_2407_18352_b200 import workloads; from oracle import c_oracle;"
+            "wl = workloads.make('minibude', 70001); wl.to_device();"
+            "got = t.run(wl, pathlib.Path(tempfile.mkdtemp()));"
+            "x = np.ascontiguousarray(wl.arrays['poses'].T); ref, _ = c_oracle.mlp_f32(wl.layers, x);"
+            "t.check_tol(got, ref[:, 0].astype(np.float64));"
+            "emu = t.emulate(wl.layers, x)[:, 0];"
+            "assert np.max(np.abs(got - emu)) <= 2e-3 * max(1.0, np.abs(emu).max()); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "SMLRT_WIDE_L1": "tc"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
