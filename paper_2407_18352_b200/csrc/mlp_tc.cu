@@ -49,6 +49,17 @@ constexpr int NTHREADS = (WARP_MMA + 1) * 32;
 #define SMLRT_LDEPTH 2
 #endif
 constexpr int LDEPTH = SMLRT_LDEPTH;  // X tiles of global loads in flight per loader thread
+#ifndef SMLRT_L2DUAL
+#define SMLRT_L2DUAL 0
+#endif
+// SMLRT_L2DUAL=1 (single-CTA kernel): layer 2's 16 K-steps alternate between
+// two TMEM accumulators summed in epilogue 2.  In isolation consecutive M=128
+// N=128 MMAs into one accumulator cost ~108 cycles each and ~64 when two
+// accumulators alternate (tools/mma_latency.cu, same operands every MMA); in
+// the kernel it measured 1.21 ms vs 1.14 ms: the two accumulators take the
+// columns of layer 2's double buffer, and the single-buffered accumulator
+// stalls the MMA warp on epilogue 2 (~500 cycles per tile).  Off by default.
+constexpr bool L2DUAL = SMLRT_L2DUAL != 0;
 
 // Biases ride on the tensor cores: a constant "ones" tile [128 x 16] (columns
 // 0 and 1 = 1.0) times a bias tile [N x 16] holding bf16(b) in k=0 and
@@ -336,9 +347,10 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
   const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 && a.staged == nullptr;
   float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
                              : nullptr;
+  constexpr bool DA = !PAIR && L2DUAL;
   for (int it = 0; it < n_my; ++it) {
-    const int b = it & 1;
-    mbar_wait(bar + L::B_L2FULL + b, (it >> 1) & 1);
+    const int b = DA ? 0 : (it & 1);
+    mbar_wait(bar + L::B_L2FULL + b, DA ? (it & 1) : ((it >> 1) & 1));
     if (q == 0 && lane == 0) TR(6, it);
     tc_fence_after();
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -346,7 +358,15 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
     for (int cc = 0; cc < H2 / 32; ++cc) {
       uint32_t v[32];
       tmem_ld32(lane_addr + b * H2 + cc * 32, v);
-      tmem_wait_ld();
+      if constexpr (DA) {
+        uint32_t w[32];
+        tmem_ld32(lane_addr + H2 + cc * 32, w);  // odd K-steps' accumulator
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(w[e]));
+      } else {
+        tmem_wait_ld();
+      }
       if (cc == H2 / 32 - 1) {
         tc_fence_before();
         arrive_mma<PAIR>(bar + L::B_L2EMPTY + b);
@@ -572,11 +592,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int b = j & 1;
       mbar_wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
       if (lane == 0) TR(11, j);
-      mbar_wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
+      if constexpr (L2DUAL)
+        mbar_wait(bar + L::B_L2EMPTY, (j & 1) ^ 1);
+      else
+        mbar_wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
       if (lane == 0) TR(1, j);
       tc_fence_after();
-      const uint32_t d = tbase + L::T_L2 + b * H2;
       const uint64_t ab = a20d + ((b * L::A2_BUF) >> 4);
+      if constexpr (L2DUAL) {
+#pragma unroll
+        for (int ks = 0; ks < 4 * L::KC; ++ks)  // even K-steps -> accumulator 0, odd -> accumulator 1
+          mma_ss_elect(tbase + L::T_L2 + (ks & 1) * H2, ab + (((ks >> 2) * L::A2_CHUNK + (ks & 3) * 32) >> 4),
+                       w20d + (((ks >> 2) * L::W2_CHUNK + (ks & 3) * 32) >> 4), idesc2, ks >= 2);
+        mma_commit_elect(bar + L::B_A2EMPTY + b);
+        mma_commit_elect(bar + L::B_L2FULL);
+        return;
+      }
+      const uint32_t d = tbase + L::T_L2 + b * H2;
 #if defined(SMLRT_ABLATE) && SMLRT_ABLATE == 2  // timing experiment only: one L2 MMA per tile
       mma_ss_elect(d, ab, w20d, idesc2, 0);
 #else
