@@ -203,6 +203,7 @@ class Runtime:
         # bench/profiling hook: CUDA events around each fused launch, on its stream
         self.time_kernels = False
         self.kernel_events: list = []
+        self._realpaths: dict = {}  # model path -> realpath (the model cache key, runtime.py:186)
 
     # -- registration ---------------------------------------------------------
 
@@ -234,7 +235,9 @@ class Runtime:
     # -- caches ---------------------------------------------------------------
 
     def _model_for(self, desc: RegionDescriptor) -> Model:
-        key = os.path.realpath(desc.ml.model_path)
+        key = self._realpaths.get(desc.ml.model_path)
+        if key is None:
+            key = self._realpaths[desc.ml.model_path] = os.path.realpath(desc.ml.model_path)
         m = self._models.get(key)
         if m is None:
             try:
@@ -257,6 +260,7 @@ class Runtime:
     def unload_models(self):
         """Drop cached models; the next inference reloads from disk."""
         self._models.clear()
+        self._realpaths.clear()
 
     def close(self):
         for db in self._dbs.values():
@@ -452,7 +456,7 @@ class Runtime:
         for m, d in zip(host_in, in_maps):
             self._staging.upload(m.array, d.array)
         for m, d in zip(host_out, out_maps):
-            if not _covers(pout, d.array):
+            if not m.array.is_device and not _covers(pout, d.array):
                 self._staging.upload(m.array, d.array)
         r0, r1 = _shard_rows(rows, self.shard)
         status = self._status_word()
