@@ -642,73 +642,51 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     (void)idesc1;
     if (n_my > 0) issue_l2(n_my - 1);
     __syncwarp();
-  } else if (warp == WARP_MMA) {
-    // ========================================================= MMA issuer
-    // (pair: rank 0 issues M = 256 MMAs over both CTAs' SMEM and TMEM)
-    if (lane == 0 && leader) {
-      constexpr uint32_t idesc1 = idesc_bf16(BM * NS, H1);
-      constexpr uint32_t idesc2 = idesc_bf16(BM * NS, H2);
-      const uint32_t w2 = smem_u32(smem + L::OFF_W2);
-      const uint32_t x0 = smem_u32(smem + L::OFF_X);
-      const uint32_t a20 = smem_u32(smem + L::OFF_A2);
-      const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
-      const uint64_t w1bd = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
-      const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
-      const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
-      auto wait = [&](uint64_t* b, uint32_t ph) {
-        if constexpr (PAIR)
-          mbar_wait_cluster(b, ph);
-        else
-          mbar_wait(b, ph);
-      };
-      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-        if constexpr (PAIR)
-          mma2_bf16(d, ad, bd, idesc, acc);
-        else
-          mma_bf16(d, ad, bd, idesc, acc);
-      };
-      auto commit = [&](uint64_t* b) {
-        if constexpr (PAIR)
-          mma2_commit_mc(b, 0x3);
-        else
-          mma_commit(b);
-      };
-      auto issue_l2 = [&](int j) {
-        const int b = j & 1;
-        wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
-        TR(11, j);
-        wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
-        TR(1, j);
-        tc_fence_after();
-        const uint32_t d = tbase + L::T_L2 + b * H2;
-        if constexpr (PAIR) mma(d, onesd, w2bd, idesc2, 0);  // D = b2 (single CTA: + b2 in epilogue 2)
+  } else if (warp == WARP_MMA && PAIR && leader) {
+    // ================================================ MMA issuer (CTA pair)
+    // rank 0's whole warp runs the loop, elect.sync issues M = 256 MMAs over
+    // both CTAs' SMEM and TMEM (same reasoning as the single-CTA issuer)
+    constexpr uint32_t idesc1 = idesc_bf16(BM * NS, H1);
+    constexpr uint32_t idesc2 = idesc_bf16(BM * NS, H2);
+    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
+    const uint64_t w1bd = smem_desc(smem_u32(smem + L::OFF_W1B), 256, kSwizzle32);
+    const uint64_t w2bd = smem_desc(smem_u32(smem + L::OFF_W2B), 256, kSwizzle32);
+    const uint64_t onesd = smem_desc(smem_u32(smem + L::OFF_ONES), 256, kSwizzle32);
+    const uint64_t x0d = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
+    const uint64_t a20d = smem_desc(smem_u32(smem + L::OFF_A2), 1024, kSwizzle128);
+    const uint64_t w20d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
+    auto issue_l2 = [&](int j) {
+      const int b = j & 1;
+      mbar_wait_cluster(bar + L::B_A2FULL + b, (j >> 1) & 1);
+      mbar_wait_cluster(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tbase + L::T_L2 + b * H2;
+      const uint64_t ab = a20d + ((b * L::A2_BUF) >> 4);
+      mma2_ss_elect(d, onesd, w2bd, idesc2, 0);  // D = b2
 #pragma unroll
-        for (int kc = 0; kc < L::KC; ++kc)
+      for (int kc = 0; kc < L::KC; ++kc)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = smem_desc(a20 + b * L::A2_BUF + kc * L::A2_CHUNK + k * 32, 1024, kSwizzle128);
-            const uint64_t bd = smem_desc(w2 + kc * L::W2_CHUNK + k * 32, 1024, kSwizzle128);
-            mma(d, ad, bd, idesc2, PAIR || (kc | k) != 0);
-          }
-        commit(bar + L::B_A2EMPTY + b);
-        commit(bar + L::B_L2FULL + b);
-      };
-      for (int it = 0; it < n_my; ++it) {
-        const int s = it % XSTAGES;
-        wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
-        TR(9, it);
-        wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
-        TR(0, it);
-        tc_fence_after();
-        if constexpr (PAIR) mma(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1 (single CTA: epilogue 1)
-        mma(tbase + L::T_L1, smem_desc(x0 + s * L::X_STAGE, 256, kSwizzle32), w1d, idesc1, PAIR ? 1 : 0);
-        commit(bar + L::B_XEMPTY + s);
-        commit(bar + L::B_L1FULL);
-        if (it > 0) issue_l2(it - 1);
-      }
-      if (n_my > 0) issue_l2(n_my - 1);
+        for (int k = 0; k < 4; ++k)
+          mma2_ss_elect(d, ab + ((kc * L::A2_CHUNK + k * 32) >> 4), w20d + ((kc * L::W2_CHUNK + k * 32) >> 4), idesc2,
+                        1);
+      mma2_commit_mc_elect(bar + L::B_A2EMPTY + b, 0x3);
+      mma2_commit_mc_elect(bar + L::B_L2FULL + b, 0x3);
+    };
+    for (int it = 0; it < n_my; ++it) {
+      const int s = it % XSTAGES;
+      mbar_wait_cluster(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
+      mbar_wait_cluster(bar + L::B_L1EMPTY, (it & 1) ^ 1);
+      tc_fence_after();
+      mma2_ss_elect(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1
+      mma2_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d, idesc1, 1);
+      mma2_commit_mc_elect(bar + L::B_XEMPTY + s, 0x3);
+      mma2_commit_mc_elect(bar + L::B_L1FULL, 0x3);
+      if (it > 0) issue_l2(it - 1);
     }
+    if (n_my > 0) issue_l2(n_my - 1);
     __syncwarp();
+  } else if (warp == WARP_MMA) {
+    // pair rank 1: its MMA warp idles (rank 0 issues for both CTAs)
   } else if (warp >= WARP_EPI1 && !PAIR) {
     const int part = (warp - WARP_EPI1) >> 2;
     if (a.act1 == SMLRT_RELU)
@@ -1173,7 +1151,7 @@ bool use_ts() {
 }
 
 // CTA-pair kernel (SMLRT_TC_PAIR=1); off by default: measured slower than the
-// single-CTA kernel on bonds (period 2800 vs 2390 cycles/tile, tools/tc_trace.py)
+// single-CTA kernel on bonds (1.24 ms vs 1.14 ms with the elect.sync issuer)
 bool use_pair() {
   static const int v = [] {
     const char* e = std::getenv("SMLRT_TC_PAIR");
