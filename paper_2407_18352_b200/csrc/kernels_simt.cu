@@ -467,33 +467,30 @@ inline bool plan_runs(const DevPlan& P, int run) {
   return true;
 }
 
-#ifndef SMLRT_MW_MINB
-#define SMLRT_MW_MINB 1
-#endif
 template <int... D>
 struct Tune {
-  static constexpr int R = 1, UNR = 64, RUN = 1, MINB = 1;
+  static constexpr int R = 1, UNR = 64, RUN = 1;
 };
 template <int A, int B, int C>
 struct Tune<A, B, C> {
-  static constexpr int R = 2, UNR = B, RUN = 1, MINB = 1;
+  static constexpr int R = 2, UNR = B, RUN = 1;
 };
 template <int A, int B, int C, int E>
 struct Tune<A, B, C, E> {
-  static constexpr int R = 2, UNR = B, RUN = 1, MINB = 1;
+  static constexpr int R = 2, UNR = B, RUN = 1;
 };
 template <>
 struct Tune<5, 64, 32, 1> {  // C1: [k, 0:5] rows
-  static constexpr int R = 2, UNR = SMLRT_OPT_UNR, RUN = 5, MINB = 1;
+  static constexpr int R = 2, UNR = SMLRT_OPT_UNR, RUN = 5;
 };
 template <>
 struct Tune<36, 8, 4> {  // C5: 3x3x4 halo = 12 runs of 3
-  static constexpr int R = 2, UNR = 8, RUN = 3, MINB = SMLRT_MW_MINB;
+  static constexpr int R = 2, UNR = 8, RUN = 3;
 };
 
 // R rows per thread (rows blockIdx*128*R + threadIdx + 128 r: coalesced per r)
 template <bool F32, int ACT1, int R, int UNR, int RUN, class S, int... D>
-__global__ void __launch_bounds__(128, Tune<D...>::MINB) region_exact_kernel(
+__global__ void __launch_bounds__(128) region_exact_kernel(
     const ModelParams<S::NPARAM, S::L> mp, const __grid_constant__ DevPlan Pin,
     const __grid_constant__ Ptrs src, const __grid_constant__ DevPlan Pout,
     const __grid_constant__ Ptrs dst, int64_t r0, int64_t r1, float* __restrict__ staged, uint32_t* status) {
