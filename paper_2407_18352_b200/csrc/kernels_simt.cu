@@ -216,15 +216,16 @@ struct Shape<A, B> {
   static constexpr int SW = r4(A), OB = B * SW;
   static constexpr int NPARAM = OB + r4(B);
 };
-// 2 layers, streamed over a row pair: P1[f] = {W1[f][0..A), b1[f]}, each value
-// duplicated (w, w) for the row-paired f32x2 ops, padded to S1 = r4(2(A+1));
+// 2 layers, streamed over a row pair: P1[f/2] = {(W1[f][i], W1[f+1][i]) for
+// i < A, (b1[f], b1[f+1])} -- hidden-unit pairs for output-paired f32x2 ops --
+// padded to S1 = r4(2(A+1));
 // P2[f] = {W2[0..C)[f]} (a column of W2, output-paired) padded to S2 = r4(C);
 // b2 [r4(C)]
 template <int A, int B, int C>
 struct Shape<A, B, C> {
   static constexpr int L = 2, IN = A, OUT = C;
   static constexpr int S1 = r4(2 * (A + 1)), S2 = r4(C);
-  static constexpr int O2 = B * S1, OB2 = O2 + B * S2;
+  static constexpr int O2 = (B / 2) * S1, OB2 = O2 + B * S2;
   static constexpr int NPARAM = OB2 + r4(C);
 };
 // 3 layers: as above, then W3 [E][r4(C)] row-major, b3 [r4(E)]
@@ -232,7 +233,7 @@ template <int A, int B, int C, int E>
 struct Shape<A, B, C, E> {
   static constexpr int L = 3, IN = A, OUT = E;
   static constexpr int S1 = r4(2 * (A + 1)), S2 = r4(C), S3 = r4(C);
-  static constexpr int O2 = B * S1, OB2 = O2 + B * S2, O3 = OB2 + r4(C), OB3 = O3 + E * S3;
+  static constexpr int O2 = (B / 2) * S1, OB2 = O2 + B * S2, O3 = OB2 + r4(C), OB3 = O3 + E * S3;
   static constexpr int NPARAM = OB3 + r4(E);
 };
 
@@ -312,44 +313,50 @@ __device__ __forceinline__ float act_c(float y) {
 template <int ACT1, int A, int B, int C, int S1, int S2, int UNR>
 __device__ __forceinline__ void layers12_streamed(const float* P1, const float* P2, const float* b2, int act2,
                                                   uint64_t one, const float (&x)[2][A], float (&y)[2][C]) {
-  static_assert(C % 2 == 0, "output-paired layer 2 needs an even width");
-  uint64_t xp[A];
-#pragma unroll
-  for (int i = 0; i < A; ++i) xp[i] = pk2(x[0][i], x[1][i]);
+  static_assert(C % 2 == 0 && B % 2 == 0, "output-paired layers need even widths");
   uint64_t acc[2][C / 2];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int j = 0; j < C / 2; ++j) acc[r][j] = 0ull;
   // partial unroll keeps the loop body inside the instruction cache (a fully
-  // unrolled 5-64-32 body stalls on instruction fetch); f stays warp-uniform,
+  // unrolled 5-64-32 body stalls on instruction fetch); fp stays warp-uniform,
   // so the weights are still fetched as uniform LDCU.128s
-#pragma unroll UNR
-  for (int f = 0; f < B; ++f) {
-    // explicit 16-byte weight fetches: the compiler cannot prove the alignment
-    // of P1 + f * S1 under the partial unroll and would issue 8-byte LDCUs
+#pragma unroll (UNR / 2 > 0 ? UNR / 2 : 1)
+  for (int fp = 0; fp < B / 2; ++fp) {
+    // layer 1 for hidden units (2fp, 2fp+1) of both rows: (x, x) * (W1[2fp][i], W1[2fp+1][i]);
+    // explicit 16-byte weight fetches (the compiler cannot prove the alignment
+    // of P1 + fp * S1 under the partial unroll and would issue 8-byte LDCUs)
     uint64_t w1[S1 / 2];
 #pragma unroll
     for (int i = 0; i < S1 / 4; ++i) {
-      const ulonglong2 q = ldw4(P1 + f * S1 + 4 * i);
+      const ulonglong2 q = ldw4(P1 + fp * S1 + 4 * i);
       w1[2 * i] = q.x;
       w1[2 * i + 1] = q.y;
     }
-    uint64_t h = 0ull;
+    float h[2][2];
 #pragma unroll
-    for (int i = 0; i < A; ++i) h = add2(h, mul2(xp[i], w1[i]), one);
-    h = add2(h, w1[A], one);  // + b1[f]
-    float ha, hb;
-    upk2(h, ha, hb);
-    ha = act_c<ACT1>(ha);
-    hb = act_c<ACT1>(hb);
-    const uint64_t hha = pk2(ha, ha), hhb = pk2(hb, hb);
+    for (int r = 0; r < 2; ++r) {
+      uint64_t hp = 0ull;
 #pragma unroll
-    for (int j = 0; j < C / 2; ++j) {
-      const ulonglong2 q = ldw4(P2 + f * S2 + 4 * (j / 2));
-      const uint64_t w = (j & 1) ? q.y : q.x;
-      acc[0][j] = add2(acc[0][j], mul2(hha, w), one);
-      acc[1][j] = add2(acc[1][j], mul2(hhb, w), one);
+      for (int i = 0; i < A; ++i) hp = add2(hp, mul2(pk2(x[r][i], x[r][i]), w1[i]), one);
+      hp = add2(hp, w1[A], one);  // + (b1[2fp], b1[2fp+1])
+      upk2(hp, h[r][0], h[r][1]);
+      h[r][0] = act_c<ACT1>(h[r][0]);
+      h[r][1] = act_c<ACT1>(h[r][1]);
+    }
+    // layer 2, output pairs, hidden units in ascending order
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int f = 2 * fp + u;
+      const uint64_t hha = pk2(h[0][u], h[0][u]), hhb = pk2(h[1][u], h[1][u]);
+#pragma unroll
+      for (int j = 0; j < C / 2; ++j) {
+        const ulonglong2 q = ldw4(P2 + f * S2 + 4 * (j / 2));
+        const uint64_t w = (j & 1) ? q.y : q.x;
+        acc[0][j] = add2(acc[0][j], mul2(hha, w), one);
+        acc[1][j] = add2(acc[1][j], mul2(hhb, w), one);
+      }
     }
   }
 #pragma unroll
@@ -402,8 +409,9 @@ template <int A, int B, int C>
 void pack12(const float* hp, float* w, int S1, int S2, int O2, int OB2) {
   const float *W1 = hp, *b1 = W1 + A * B, *W2 = b1 + B, *b2 = W2 + B * C;
   for (int f = 0; f < B; ++f) {
-    for (int i = 0; i < A; ++i) w[f * S1 + 2 * i] = w[f * S1 + 2 * i + 1] = W1[f * A + i];
-    w[f * S1 + 2 * A] = w[f * S1 + 2 * A + 1] = b1[f];
+    const int fp = f / 2, u = f % 2;  // hidden-unit pair, slot within the pair
+    for (int i = 0; i < A; ++i) w[fp * S1 + 2 * i + u] = W1[f * A + i];
+    w[fp * S1 + 2 * A + u] = b1[f];
     for (int j = 0; j < C; ++j) w[O2 + f * S2 + j] = W2[j * B + f];
   }
   for (int j = 0; j < C; ++j) w[OB2 + j] = b2[j];
