@@ -310,13 +310,13 @@ __device__ __forceinline__ float act_c(float y) {
 // pairs (x_a[i], x_b[i]) x (w, w) with duplicated weights; layer 2 on output
 // pairs (h, h) x (W2[j, f], W2[j+1, f]).  Each FMUL2/FFMA2 does the work of
 // two FMUL/FADD, halving the issue slots of the (issue-bound) kernel.
-template <int ACT1, int A, int B, int C, int S1, int S2, int UNR>
+template <int ACT1, int A, int B, int C, int S1, int S2, int UNR, int R>
 __device__ __forceinline__ void layers12_streamed(const float* P1, const float* P2, const float* b2, int act2,
-                                                  uint64_t one, const float (&x)[2][A], float (&y)[2][C]) {
+                                                  uint64_t one, const float (&x)[R][A], float (&y)[R][C]) {
   static_assert(C % 2 == 0 && B % 2 == 0, "output-paired layers need even widths");
-  uint64_t acc[2][C / 2];
+  uint64_t acc[R][C / 2];
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int j = 0; j < C / 2; ++j) acc[r][j] = 0ull;
   // partial unroll keeps the loop body inside the instruction cache (a fully
@@ -324,7 +324,7 @@ __device__ __forceinline__ void layers12_streamed(const float* P1, const float* 
   // so the weights are still fetched as uniform LDCU.128s
 #pragma unroll (UNR / 2 > 0 ? UNR / 2 : 1)
   for (int fp = 0; fp < B / 2; ++fp) {
-    // layer 1 for hidden units (2fp, 2fp+1) of both rows: (x, x) * (W1[2fp][i], W1[2fp+1][i]);
+    // layer 1 for hidden units (2fp, 2fp+1): (x, x) * (W1[2fp][i], W1[2fp+1][i]);
     // explicit 16-byte weight fetches (the compiler cannot prove the alignment
     // of P1 + fp * S1 under the partial unroll and would issue 8-byte LDCUs)
     uint64_t w1[S1 / 2];
@@ -334,9 +334,9 @@ __device__ __forceinline__ void layers12_streamed(const float* P1, const float* 
       w1[2 * i] = q.x;
       w1[2 * i + 1] = q.y;
     }
-    float h[2][2];
+    float h[R][2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < R; ++r) {
       uint64_t hp = 0ull;
 #pragma unroll
       for (int i = 0; i < A; ++i) hp = add2(hp, mul2(pk2(x[r][i], x[r][i]), w1[i]), one);
@@ -349,18 +349,17 @@ __device__ __forceinline__ void layers12_streamed(const float* P1, const float* 
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int f = 2 * fp + u;
-      const uint64_t hha = pk2(h[0][u], h[0][u]), hhb = pk2(h[1][u], h[1][u]);
 #pragma unroll
       for (int j = 0; j < C / 2; ++j) {
         const ulonglong2 q = ldw4(P2 + f * S2 + 4 * (j / 2));
         const uint64_t w = (j & 1) ? q.y : q.x;
-        acc[0][j] = add2(acc[0][j], mul2(hha, w), one);
-        acc[1][j] = add2(acc[1][j], mul2(hhb, w), one);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r][j] = add2(acc[r][j], mul2(pk2(h[r][u], h[r][u]), w), one);
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int j = 0; j < C / 2; ++j) {
       float lo, hi;
@@ -381,17 +380,16 @@ template <int ACT1, int R, int UNR, int A, int B, int C>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C>::NPARAM, 2>& mp,
                                         const float (&x)[R][A], float (&y)[R][C]) {
   using S = Shape<A, B, C>;
-  static_assert(R == 2, "2/3-layer shapes run on row pairs");
-  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x, y);
+  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR, R>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x,
+                                                         y);
 }
 template <int ACT1, int R, int UNR, int A, int B, int C, int E>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C, E>::NPARAM, 3>& mp,
                                         const float (&x)[R][A], float (&y)[R][E]) {
   using S = Shape<A, B, C, E>;
-  static_assert(R == 2, "2/3-layer shapes run on row pairs");
   float h2[R][C];
-  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x,
-                                                      h2);
+  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR, R>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x,
+                                                         h2);
 #pragma unroll
   for (int r = 0; r < R; ++r) layer_exact<C, E, S::S3>(h2[r], y[r], mp.w + S::O3, mp.w + S::OB3, mp.act[2]);
 }
@@ -488,12 +486,18 @@ struct Tune<A, B, C, E> {
   static constexpr int R = 2, UNR = B, RUN = 1;
 };
 template <>
+#ifndef SMLRT_OPT_R
+#define SMLRT_OPT_R 2
+#endif
 struct Tune<5, 64, 32, 1> {  // C1: [k, 0:5] rows
-  static constexpr int R = 2, UNR = SMLRT_OPT_UNR, RUN = 5;
+  static constexpr int R = SMLRT_OPT_R, UNR = SMLRT_OPT_UNR, RUN = 5;
 };
 template <>
+#ifndef SMLRT_MW_R
+#define SMLRT_MW_R 1
+#endif
 struct Tune<36, 8, 4> {  // C5: 3x3x4 halo = 12 runs of 3
-  static constexpr int R = 2, UNR = 8, RUN = 3;
+  static constexpr int R = SMLRT_MW_R, UNR = 8, RUN = 3;
 };
 
 // R rows per thread (rows blockIdx*128*R + threadIdx + 128 r: coalesced per r)
