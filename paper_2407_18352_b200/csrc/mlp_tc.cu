@@ -27,6 +27,16 @@
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
+// SMLRT_SLEEPWAIT=1: every mbarrier wait in this file carries a suspend-time
+// hint, so waiting warps (the MMA issuer above all) stop re-polling and leave
+// their sub-partition's issue slots to the epilogue warps sharing it
+#ifndef SMLRT_SLEEPWAIT
+#define SMLRT_SLEEPWAIT 0
+#endif
+#if SMLRT_SLEEPWAIT
+#define mbar_wait mbar_wait_sleep
+#endif
+
 namespace smlrt {
 namespace {
 
