@@ -136,3 +136,26 @@ def test_bf16_relu_propagates_nan(cuda, tmp_path):
             rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "m"))))
     got = wl.buffers["val"].to_numpy()
     assert np.isnan(got[1234]) and np.isfinite(np.delete(got, 1234)).all()
+
+
+@pytest.mark.parametrize("env", [{"SMLRT_TC_KERNEL": "ts"}, {"SMLRT_TC_KERNEL": "ts2"}, {"SMLRT_TC_PAIR": "1"}])
+def test_bonds_kernel_variants(cuda, env):
+    """The opt-in bonds kernels (TMEM A operand, TS2, CTA pair) meet the same
+    tolerances; each runs in a subprocess because the switches are read once."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, pathlib, tempfile, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "import test_gpu_tc as t; import paper_2407_18352_b200 as sm;"
+            "from paper_2407_18352_b200 import workloads; from oracle import c_oracle;"
+            "wl = workloads.make('bonds', 148 * 128 * 3 + 77); wl.to_device();"
+            "d = pathlib.Path(tempfile.mkdtemp()); sm.save_model(wl.model, d / 'm');"
+            "rt = sm.Runtime(); rt.invoke_region(rt.register_region(wl.descriptor(str(d / 'm'))));"
+            "got = wl.buffers['val'].to_numpy().astype(np.float64);"
+            "ref, _ = c_oracle.mlp_f32(wl.layers, wl.arrays['bonds']); t.check_tol(got, ref[:, 0]);"
+            "emu = t.emulate_bf16(wl.layers, wl.arrays['bonds'])[:, 0];"
+            "assert np.max(np.abs(got - emu)) <= 2e-3 * max(1.0, np.abs(emu).max()); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
