@@ -299,7 +299,13 @@ __global__ void __launch_bounds__(GTHREADS, 1)
 constexpr int L12_PW = 8;  // producer warps: 2 per SM sub-partition (latency hiding)
 template <int NH>
 constexpr int l12_threads() { return 32 * (2 + 4 * NH + L12_PW); }
-constexpr int L12_SA = 3, L12_SB = 4;
+#ifndef SMLRT_L12_SA
+#define SMLRT_L12_SA 3
+#endif
+#ifndef SMLRT_L12_SB
+#define SMLRT_L12_SB 4
+#endif
+constexpr int L12_SA = SMLRT_L12_SA, L12_SB = SMLRT_L12_SB;  // A ring (on-chip layer 1), B ring (TMA W2 boxes)
 constexpr int L12_H1MAX = 1024;
 
 template <int NH>
@@ -1125,7 +1131,14 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
   const __nv_bfloat16* W2 = W1p + (size_t)h1 * 16;
   const __nv_bfloat16* W3 = W2 + (size_t)h2 * h1;
   const int64_t rows = r1 - r0;
-  const int64_t ch = std::min<int64_t>(rows, 1 << 20);
+  // rows per block: the layer-2 activations of a block round-trip HBM
+  // ([rows x H2] bf16); SMLRT_WIDE_BLOCK overrides the default 2^22 (measured: 2^19 / 2^20 / 2^21 / 2^22 rows -> 94.4 / 93.0 / 92.2 / 91.1 ms per C3 step)
+  static const int64_t block_rows = [] {
+    const char* e = std::getenv("SMLRT_WIDE_BLOCK");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? (int64_t)v : (int64_t)(1 << 22);
+  }();
+  const int64_t ch = std::min<int64_t>(rows, block_rows);
   const bool fused12 = l12_shape(m) && in.n_cols == F && F <= SMLRT_INLINE_COLS && !l12_disabled();
   __nv_bfloat16* buf;
   SMLRT_CUDA(cudaMallocAsync(&buf, (size_t)ch * (fused12 ? h2 : 16 + h1 + h2) * 2, s));
