@@ -30,6 +30,9 @@
 // SMLRT_SLEEPWAIT=1: every mbarrier wait in this file carries a suspend-time
 // hint, so waiting warps (the MMA issuer above all) stop re-polling and leave
 // their sub-partition's issue slots to the epilogue warps sharing it
+#ifndef SMLRT_LDX64
+#define SMLRT_LDX64 1
+#endif
 #ifndef SMLRT_SLEEPWAIT
 #define SMLRT_SLEEPWAIT 0
 #endif
@@ -302,9 +305,14 @@ __device__ __forceinline__ void epilogue1_split(uint8_t* smem, uint64_t* bar, ui
       // columns at once; only then wait for the A2 buffer (which frees when
       // layer 2 of tile it-2 completes)
       uint32_t v[HC];
+#if SMLRT_LDX64
+      if constexpr (HC == 64)
+        tmem_ld64(tbase + lane_off + L::T_L1 + col0, v);
+      else
+#endif
 #pragma unroll
-      for (int c = 0; c < HC / 16; ++c)
-        tmem_ld16(tbase + lane_off + L::T_L1 + col0 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
+        for (int c = 0; c < HC / 16; ++c)
+          tmem_ld16(tbase + lane_off + L::T_L1 + col0 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar + (h == 0 ? L::B_L1EMPTY : L::B_L1EMPTY2));
@@ -364,6 +372,30 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
     if (q == 0 && lane == 0) TR(6, it);
     tc_fence_after();
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#if SMLRT_LDX64
+    if constexpr (!PAIR && !DA && H2 % 64 == 0) {
+      // 64 columns per TMEM request, half the wait points of the x32 loop
+#pragma unroll
+      for (int c2 = 0; c2 < H2 / 64; ++c2) {
+        uint32_t v[64];
+        tmem_ld64(lane_addr + b * H2 + c2 * 64, v);
+        tmem_wait_ld();
+        if (c2 == H2 / 64 - 1) {
+          tc_fence_before();
+          mbar_arrive(bar + L::B_L2EMPTY + b);
+        }
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          const float4 ww = *reinterpret_cast<const float4*>(a.w3 + c2 * 64 + e);
+          const float4 bb = *reinterpret_cast<const float4*>(a.b2 + c2 * 64 + e);
+          acc[((e >> 2) & 1) * 4 + 0] = fmaf(act_t<ACT>(__uint_as_float(v[e]) + bb.x), ww.x, acc[((e >> 2) & 1) * 4 + 0]);
+          acc[((e >> 2) & 1) * 4 + 1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1]) + bb.y), ww.y, acc[((e >> 2) & 1) * 4 + 1]);
+          acc[((e >> 2) & 1) * 4 + 2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2]) + bb.z), ww.z, acc[((e >> 2) & 1) * 4 + 2]);
+          acc[((e >> 2) & 1) * 4 + 3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3]) + bb.w), ww.w, acc[((e >> 2) & 1) * 4 + 3]);
+        }
+      }
+    } else
+#endif
 #pragma unroll
     for (int cc = 0; cc < H2 / 32; ++cc) {
       uint32_t v[32];
