@@ -830,9 +830,12 @@ __device__ __forceinline__ void epilogue1_ts(uint64_t* bar, uint32_t tbase, int 
       if (q == 0 && part == 0 && lane == 0) TR(2 + 10 * h, it);
       tc_fence_after();
       uint32_t v[NC];
+      if constexpr (NC == 64 && SMLRT_LDX64)
+        tmem_ld64(tbase + lane_off + L::T_L1 + part * NC, *reinterpret_cast<uint32_t(*)[64]>(v));
+      else
 #pragma unroll
-      for (int c = 0; c < NC / 32; ++c)
-        tmem_ld32(tbase + lane_off + L::T_L1 + part * NC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        for (int c = 0; c < NC / 32; ++c)
+          tmem_ld32(tbase + lane_off + L::T_L1 + part * NC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar + L::B_L1EMPTY);
