@@ -58,6 +58,15 @@ constexpr int XSTAGES = SMLRT_XSTAGES;
 constexpr int NP = SMLRT_EPI1_PARTS;
 constexpr int WARP_EPI2 = 0, WARP_EPI1 = 4, WARP_LOAD = 4 + 4 * NP, WARP_MMA = WARP_LOAD + 4;
 constexpr int NTHREADS = (WARP_MMA + 1) * 32;
+#ifndef SMLRT_MMA2W
+#define SMLRT_MMA2W 1
+#endif
+// SMLRT_MMA2W=1 (single-CTA SS kernel): layer 1 and layer 2 are issued by two
+// different warps, so the next tile's layer-1 MMA does not queue behind the
+// MMA warp's waits for the current tile's A2 buffer.
+constexpr int MMA2W = SMLRT_MMA2W;
+template <bool PAIR>
+constexpr int ss_threads() { return PAIR ? NTHREADS : NTHREADS + 32 * MMA2W; }
 #ifndef SMLRT_LDEPTH
 #define SMLRT_LDEPTH 2
 #endif
@@ -182,7 +191,7 @@ __device__ __forceinline__ float ld_elem(const void* base, int dt, int64_t i) {
 // Debug-only pipeline trace (build with -DSMLRT_TC_TRACE; `make trace`):
 // clock64 stamps of each role's events for the first TR_TILES tiles of CTAs 0/1.
 #ifdef SMLRT_TC_TRACE
-constexpr int TR_TILES = 64, TR_EV = 16;
+constexpr int TR_TILES = 1024, TR_EV = 16;
 __device__ unsigned long long g_tc_trace[2][TR_TILES][TR_EV];
 #define TR(ev, it)                                                   \
   do {                                                               \
@@ -339,7 +348,13 @@ __device__ __forceinline__ void epilogue1_split(uint8_t* smem, uint64_t* bar, ui
     }
     fence_async_smem();
     mbar_arrive(bar + L::B_A2FULL + b);
-    if (q == 0 && PART == 0 && lane == 0) TR(5, it);
+#ifndef SMLRT_TRACE_ALT
+#define SMLRT_TRACE_ALT 0
+#endif
+    if (q == 0 && PART == SMLRT_TRACE_ALT && lane == 0) TR(5, it);
+    if (q == 3 && PART == (1 ^ SMLRT_TRACE_ALT) && lane == 0) TR(3, it);
+    if (q == 1 && PART == (1 ^ SMLRT_TRACE_ALT) && lane == 0) TR(4, it);
+    if (q == 2 && PART == (0 ^ SMLRT_TRACE_ALT) && lane == 0) TR(10, it);
   }
 }
 
@@ -466,7 +481,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
 }
 
 template <int H1, int H2, bool PAIR>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(ss_threads<PAIR>(), 1)
     mlp3_tc_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
                    const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
                    const __grid_constant__ Ptrs8 dst) {
@@ -508,13 +523,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   {  // resident weights: this rank's blob -> smem (16-byte vectors); ones tile built here
     const int4* g = reinterpret_cast<const int4*>(a.blob + rank * L::BLOB);
-    for (int i = threadIdx.x; i < L::BLOB_W1 / 16; i += NTHREADS)
+    for (int i = threadIdx.x; i < L::BLOB_W1 / 16; i += ss_threads<PAIR>())
       reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
-    for (int i = threadIdx.x; i < (L::BLOB_TAIL - L::BLOB_W1) / 16; i += NTHREADS)
+    for (int i = threadIdx.x; i < (L::BLOB_TAIL - L::BLOB_W1) / 16; i += ss_threads<PAIR>())
       reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[L::BLOB_W1 / 16 + i];
-    for (int i = threadIdx.x; i < L::TAIL / 16; i += NTHREADS)
+    for (int i = threadIdx.x; i < L::TAIL / 16; i += ss_threads<PAIR>())
       reinterpret_cast<int4*>(smem + L::OFF_W3)[i] = g[L::BLOB_TAIL / 16 + i];
-    for (int i = threadIdx.x; i < BM * KX; i += NTHREADS) {
+    for (int i = threadIdx.x; i < BM * KX; i += ss_threads<PAIR>()) {
       const int row = i / KX, k = i % KX;
       *reinterpret_cast<__nv_bfloat16*>(smem + L::OFF_ONES + sw32_offset(row, k)) =
           __float2bfloat16_rn(k < 2 ? 1.0f : 0.0f);
@@ -616,7 +631,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
       }
     }
-  } else if (warp == WARP_MMA && !PAIR) {
+  } else if ((warp == WARP_MMA || (MMA2W && warp == WARP_MMA + 1)) && !PAIR) {
     // ========================================================= MMA issuer
     // Whole warp runs the loop (warp-uniform control flow, descriptors in
     // uniform registers), elect.sync inside the asm picks the issuing lane:
@@ -665,6 +680,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mma_commit_elect(bar + L::B_L2FULL + b);
     };
     constexpr uint32_t idesc1h = idesc_bf16(BM, H1 / 2);
+    if (MMA2W && warp == WARP_MMA + 1) {
+      for (int j = 0; j < n_my; ++j) issue_l2(j);
+      __syncwarp();
+    } else {
     for (int it = 0; it < n_my; ++it) {
       const int s = it % XSTAGES;
       mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
@@ -673,17 +692,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int h = 0; h < 2; ++h) {  // layer 1 in two halves with separate TMEM columns / barriers
         mbar_wait(bar + (h == 0 ? L::B_L1EMPTY : L::B_L1EMPTY2), (it & 1) ^ 1);
         if (lane == 0 && h == 0) TR(0, it);
+#ifdef SMLRT_TC_TRACE
+        if (lane == 0 && h == 0 && blockIdx.x < 2 && it < TR_TILES) {
+          unsigned long long ns;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+          g_tc_trace[blockIdx.x][it][15] = ns;
+        }
+#endif
         tc_fence_after();
         mma_ss_elect(tbase + L::T_L1 + h * (H1 / 2), x0d + ((s * L::X_STAGE) >> 4),
                      w1d + ((h * (H1 / 2) * 32) >> 4), idesc1h, 0);
         mma_commit_elect(bar + (h == 0 ? L::B_L1FULL : L::B_L1FULL2));
+        if (lane == 0 && h == 0) TR(14, it);
       }
       mma_commit_elect(bar + L::B_XEMPTY + s);
-      if (it > 0) issue_l2(it - 1);
+      if (lane == 0) TR(13, it);
+      if (!MMA2W && it > 0) issue_l2(it - 1);
     }
     (void)idesc1;
-    if (n_my > 0) issue_l2(n_my - 1);
+    if (!MMA2W && n_my > 0) issue_l2(n_my - 1);
     __syncwarp();
+    }
   } else if (warp == WARP_MMA && PAIR && leader) {
     // ================================================ MMA issuer (CTA pair)
     // rank 0's whole warp runs the loop, elect.sync issues M = 256 MMAs over
@@ -1645,7 +1674,7 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     }
   } else if (!pair) {
     const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-    mlp3_tc_kernel<H1, H2, false><<<grid, NTHREADS, Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
+    mlp3_tc_kernel<H1, H2, false><<<grid, ss_threads<false>(), Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
     count_launch();
   } else {
     const int pairs = (a.n_tiles + 1) / 2;
