@@ -892,7 +892,7 @@ __device__ __forceinline__ void epilogue1_ts(uint64_t* bar, uint32_t tbase, int 
 }
 
 template <int H1, int H2>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(ss_threads<false>(), 1)
     mlp3_ts_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
                    const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
                    const __grid_constant__ Ptrs8 dst) {
@@ -922,9 +922,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
   {  // resident weights: W2 chunks and W1 from the single-CTA blob
     const int4* g = reinterpret_cast<const int4*>(a.blob);
-    for (int i = threadIdx.x; i < BL::BLOB_W1 / 16; i += NTHREADS)
+    for (int i = threadIdx.x; i < BL::BLOB_W1 / 16; i += ss_threads<false>())
       reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
-    for (int i = threadIdx.x; i < H1 * 32 / 16; i += NTHREADS)
+    for (int i = threadIdx.x; i < H1 * 32 / 16; i += ss_threads<false>())
       reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[BL::BLOB_W1 / 16 + i];
   }
   fence_async_smem();
@@ -1013,8 +1013,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
       }
     }
-  } else if (warp == WARP_MMA) {
-    // whole warp, elect.sync issue (see the SS kernel)
+  } else if (warp == WARP_MMA || (MMA2W && warp == WARP_MMA + 1)) {
+    // whole warp, elect.sync issue (see the SS kernel); with MMA2W layer 1
+    // and layer 2 each have their own issuing warp
     constexpr uint32_t idesc1 = idesc_bf16(BM, H1 / 2);
     constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
     const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
@@ -1046,15 +1047,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mma_commit_elect(bar + L::B_A2EMPTY + h);
       if (h == 1) mma_commit_elect(bar + L::B_L2FULL + b);
     };
-    if (n_my > 0) {
-      l1(0, 0);
-      l1(0, 1);
-    }
-    for (int it = 0; it < n_my; ++it) {
-      l2(it, 0);
-      if (it + 1 < n_my) l1(it + 1, 0);
-      l2(it, 1);
-      if (it + 1 < n_my) l1(it + 1, 1);
+    if (MMA2W && warp == WARP_MMA) {
+      for (int it = 0; it < n_my; ++it) {
+        l1(it, 0);
+        l1(it, 1);
+      }
+    } else if (MMA2W) {
+      for (int it = 0; it < n_my; ++it) {
+        l2(it, 0);
+        l2(it, 1);
+      }
+    } else {
+      if (n_my > 0) {
+        l1(0, 0);
+        l1(0, 1);
+      }
+      for (int it = 0; it < n_my; ++it) {
+        l2(it, 0);
+        if (it + 1 < n_my) l1(it + 1, 0);
+        l2(it, 1);
+        if (it + 1 < n_my) l1(it + 1, 1);
+      }
     }
     __syncwarp();
   } else if (warp >= WARP_EPI1) {
@@ -1669,7 +1682,7 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
   } else if (!pair && use_ts() && ts_ok<H1>()) {
     if constexpr (ts_ok<H1>()) {
       const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-      mlp3_ts_kernel<H1, H2><<<grid, NTHREADS, LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
+      mlp3_ts_kernel<H1, H2><<<grid, ss_threads<false>(), LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
       count_launch();
     }
   } else if (!pair) {

@@ -193,6 +193,7 @@ class Runtime:
         self._dbs: dict[str, srdb.SrdbDatabase] = {}
         self._plans: dict[str, tuple] = {}
         self._staging = _Staging()
+        self._side = None  # (host->device, device->host) streams of the chunked host path
         self.precision = precision
         self.commit = commit
         self.shard = shard
@@ -453,6 +454,9 @@ class Runtime:
             raise ModelShapeMismatchError(
                 f"region {desc.name!r} scatters {out_counts} features, model emits {model.output_features}")
         handle = device_model(model, self.device, self.precision)
+        if self._streamable(desc, host_in, host_out, pin, pout, rows):
+            return self._run_streamed(st, host_in[0], in_maps[0], host_out[0], out_maps[0], pin, pout, rows,
+                                      handle, _ns_since(t0))
         for m, d in zip(host_in, in_maps):
             self._staging.upload(m.array, d.array)
         for m, d in zip(host_out, out_maps):
@@ -505,6 +509,62 @@ class Runtime:
                              elapsed_map_to_ns=map_to, elapsed_map_from_ns=map_from,
                              elapsed_infer_ns=infer_ns)
 
+    # host-resident (pinned) row-major input and output: the row range is cut
+    # into chunks whose host->device copy, kernel and device->host copy run on
+    # three streams, so the PCIe transfers overlap the kernel and each other
+    STREAM_MIN_ROWS = 1 << 18
+    STREAM_CHUNK_ROWS = 1 << 17   # minimum rows per chunk; at most STREAM_CHUNKS chunks
+    STREAM_CHUNKS = 16
+
+    def _streamable(self, desc, host_in, host_out, pin, pout, rows) -> bool:
+        if self.time_kernels or self.commit != "fused" or rows < self.STREAM_MIN_ROWS or desc.inout_maps:
+            return False
+        if len(host_in) != 1 or len(host_out) != 1:
+            return False
+        for m, plan in ((host_in[0], pin), (host_out[0], pout)):
+            if m.array.is_device or not m.array.data.is_pinned() or not _row_major(plan):
+                return False
+        return True
+
+    def _run_streamed(self, st, hin_map, din_map, hout_map, dout_map, pin, pout, rows, handle, map_to):
+        t0 = time.perf_counter_ns()
+        r0, r1 = _shard_rows(rows, self.shard)
+        cs = torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+        up, down = self._side
+        status = self._status_word()
+        status.zero_()
+        hin, din = hin_map.array.data.view(-1), din_map.array.data.view(-1)
+        hout, dout = hout_map.array.data.view(-1), dout_map.array.data.view(-1)
+        ci, co = pin.n_cols, pout.n_cols
+        iptr, idt = pin.ptrs_and_dtypes()
+        optr, odt = pout.ptrs_and_dtypes()
+        up.wait_stream(cs)      # the mirrors may still be read/written by earlier work
+        down.wait_stream(cs)
+        step = max(self.STREAM_CHUNK_ROWS, -(-(r1 - r0) // self.STREAM_CHUNKS))
+        for a in range(r0, r1, step):
+            b = min(r1, a + step)
+            with torch.cuda.stream(up):
+                din[a * ci:b * ci].copy_(hin[a * ci:b * ci], non_blocking=True)
+            cs.wait_stream(up)
+            _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, a, b,
+                                 _native.COMMIT_FUSED, None, cs.cuda_stream, status.data_ptr())
+            down.wait_stream(cs)
+            with torch.cuda.stream(down):
+                hout[a * co:b * co].copy_(dout[a * co:b * co], non_blocking=True)
+        cs.wait_stream(down)
+        bad = int(status.item())  # synchronises the stream
+        infer_ns = _ns_since(t0)
+        if bad:
+            raise NonFiniteOutputError("forward pass produced NaN/inf")
+        st.surrogate_calls += 1
+        st.map_to_ns += map_to
+        st.infer_ns += infer_ns
+        return RegionOutcome(path_taken=SURROGATE, elapsed_region_ns=infer_ns,
+                             elapsed_map_to_ns=map_to, elapsed_map_from_ns=0,
+                             elapsed_infer_ns=infer_ns)
+
     def stats(self, handle: str) -> RegionStats:
         self._region(handle)
         return replace(self._stats[handle])
@@ -534,6 +594,16 @@ def _flat_plan(groups, direction):
                                  (strides[-1],) + v.strides[v.n_sweep:], 1))
         flat.append(fv)
     return build_plan(flat, direction)
+
+
+def _row_major(plan: Plan) -> bool:
+    """True when plan row r touches exactly elements [r*n_cols, (r+1)*n_cols)
+    of the plan's single array (so a row range is one contiguous byte range)."""
+    if len(plan.arrays) != 1:
+        return False
+    info = _native.plan_info(plan.handle)
+    return bool(info["dense_rows"]) and info["row_pitch"] == plan.n_cols and \
+        plan.n_rows * plan.n_cols == plan.arrays[0].data.numel()
 
 
 def _covers(plan: Plan, array: ArrayBuffer) -> bool:

@@ -243,3 +243,43 @@ def test_status_word_resets_between_calls(cuda, tmp_path, jdir):
             assert rt.invoke_region(hg).path_taken == "surrogate"
             with pytest.raises(NonFiniteOutputError):
                 rt.invoke_region(hb)
+
+
+@pytest.mark.parametrize("config,shard", [("bonds", None), ("bonds", (1, 3)), ("options", None)])
+def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, shard):
+    """Pinned host input/output with row-major plans take the chunked
+    three-stream path (H2D / kernel / D2H overlapped); results are bitwise
+    those of the device-resident call, including a ragged last chunk."""
+    from paper_2407_18352_b200 import workloads
+    n = 20 * sm.Runtime.STREAM_CHUNK_ROWS + 12345
+    dev_wl = workloads.make(config, n)
+    dev_wl.to_device()
+    host_wl = workloads.make(config, n)
+    host_wl.to_device(pinned_host=True)
+    sm.save_model(dev_wl.model, tmp_path / "m")
+    with sm.Runtime(shard=shard) as rt:
+        rt.invoke_region(rt.register_region(dev_wl.descriptor(str(tmp_path / "m"))))
+        hd = host_wl.descriptor(str(tmp_path / "m"), name="host")
+        plans_before = len(rt._plans)
+        rt.invoke_region(rt.register_region(hd))
+        assert rt._side is not None, "chunked path not taken"
+        assert len(rt._plans) == plans_before + 1
+    _, _, _, to = dev_wl.functors()
+    got = host_wl.buffers[to.array].data.numpy()
+    want = dev_wl.buffers[to.array].data.cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_chunked_host_path_nonfinite(cuda, tmp_path):
+    from paper_2407_18352_b200 import workloads
+    n = sm.Runtime.STREAM_MIN_ROWS + 7
+    wl = workloads.make("bonds", n)
+    wl.to_device(pinned_host=True)
+    fi, fo, ti, to = wl.functors()
+    wl.buffers[ti.array].data[-16:] = float("inf")  # last row of the last chunk
+    sm.save_model(wl.model, tmp_path / "m")
+    with sm.Runtime() as rt:
+        h = rt.register_region(wl.descriptor(str(tmp_path / "m")))
+        with pytest.raises(NonFiniteOutputError):
+            rt.invoke_region(h)
+        assert rt._side is not None
