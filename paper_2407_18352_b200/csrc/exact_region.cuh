@@ -188,6 +188,67 @@ __device__ __forceinline__ void layers12_streamed(const float* P1, const float* 
     }
 }
 
+// Input-outer order for narrow hidden layers (C5: 36-8-4): for each input i
+// the B/2 hidden-pair accumulators advance together, so only x and B/2 packed
+// accumulators are live (not a hidden pair's whole weight row) -- fewer
+// registers, more resident warps.  Per hidden unit the operation sequence is
+// unchanged (i ascending, bias last; layer 2 f ascending): bitwise identical
+// to layers12_streamed.
+template <int ACT1, int A, int B, int C, int S1, int S2, int R>
+__device__ __forceinline__ void layers12_io(const float* P1, const float* P2, const float* b2, int act2,
+                                            uint64_t one, const float (&x)[R][A], float (&y)[R][C]) {
+  static_assert(C % 2 == 0 && B % 2 == 0, "output-paired layers need even widths");
+  uint64_t hp[R][B / 2];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int p = 0; p < B / 2; ++p) hp[r][p] = 0ull;
+#pragma unroll
+  for (int i = 0; i < A; ++i)
+#pragma unroll
+    for (int p = 0; p < B / 2; ++p) {
+      const uint64_t w = ldw2(P1 + p * S1 + 2 * i);
+#pragma unroll
+      for (int r = 0; r < R; ++r) hp[r][p] = add2(hp[r][p], mul2(pk2(x[r][i], x[r][i]), w), one);
+    }
+  float h[R][B];
+#pragma unroll
+  for (int p = 0; p < B / 2; ++p) {
+    const uint64_t bb = ldw2(P1 + p * S1 + 2 * A);  // (b1[2p], b1[2p+1])
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      upk2(add2(hp[r][p], bb, one), h[r][2 * p], h[r][2 * p + 1]);
+      h[r][2 * p] = act_c<ACT1>(h[r][2 * p]);
+      h[r][2 * p + 1] = act_c<ACT1>(h[r][2 * p + 1]);
+    }
+  }
+  uint64_t acc[R][C / 2];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C / 2; ++j) acc[r][j] = 0ull;
+#pragma unroll
+  for (int f = 0; f < B; ++f)
+#pragma unroll
+    for (int j = 0; j < C / 2; ++j) {
+      const uint64_t w = ldw2(P2 + f * S2 + 2 * j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r][j] = add2(acc[r][j], mul2(pk2(h[r][f], h[r][f]), w), one);
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C / 2; ++j) {
+      float lo, hi;
+      upk2(add2(acc[r][j], ldw2(b2 + 2 * j), one), lo, hi);
+      y[r][2 * j] = activate(lo, act2);
+      y[r][2 * j + 1] = activate(hi, act2);
+    }
+}
+
+template <int A, int B, int C>
+constexpr bool io_order();
+
 template <int ACT1, int R, int UNR, int A, int B>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B>::NPARAM, 1>& mp,
                                         const float (&x)[R][A], float (&y)[R][B]) {
@@ -199,8 +260,11 @@ template <int ACT1, int R, int UNR, int A, int B, int C>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C>::NPARAM, 2>& mp,
                                         const float (&x)[R][A], float (&y)[R][C]) {
   using S = Shape<A, B, C>;
-  layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR, R>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x,
-                                                         y);
+  if constexpr (io_order<A, B, C>())
+    layers12_io<ACT1, A, B, C, S::S1, S::S2, R>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x, y);
+  else
+    layers12_streamed<ACT1, A, B, C, S::S1, S::S2, UNR, R>(mp.w, mp.w + S::O2, mp.w + S::OB2, mp.act[1], mp.one2, x,
+                                                           y);
 }
 template <int ACT1, int R, int UNR, int A, int B, int C, int E>
 __device__ __forceinline__ void forward(const ModelParams<Shape<A, B, C, E>::NPARAM, 3>& mp,
@@ -299,6 +363,7 @@ struct Tune {
 template <int A, int B, int C>
 struct Tune<A, B, C> {
   static constexpr int R = 2, UNR = B, RUN = 1;
+  static constexpr bool IO = false;
 };
 template <int A, int B, int C, int E>
 struct Tune<A, B, C, E> {
@@ -315,13 +380,26 @@ template <>
 #ifndef SMLRT_MW_R
 #define SMLRT_MW_R 1
 #endif
+#ifndef SMLRT_MW_IO
+#define SMLRT_MW_IO 1
+#endif
 struct Tune<36, 8, 4> {  // C5: 3x3x4 halo = 12 runs of 3
   static constexpr int R = SMLRT_MW_R, UNR = 8, RUN = 3;
+  static constexpr bool IO = SMLRT_MW_IO;
 };
+template <int A, int B, int C>
+constexpr bool io_order() { return Tune<A, B, C>::IO; }
 
 // R rows per thread (rows blockIdx*128*R + threadIdx + 128 r: coalesced per r)
+// a translation unit may set SMLRT_EXACT_MINB (resident CTAs per SM) to cap
+// the register allocation of its instantiations
+#ifdef SMLRT_EXACT_MINB
+#define SMLRT_EXACT_LB __launch_bounds__(128, SMLRT_EXACT_MINB)
+#else
+#define SMLRT_EXACT_LB __launch_bounds__(128)
+#endif
 template <bool F32, int ACT1, int R, int UNR, int RUN, class S, int... D>
-__global__ void __launch_bounds__(128) region_exact_kernel(
+__global__ void SMLRT_EXACT_LB region_exact_kernel(
     const ModelParams<S::NPARAM, S::L> mp, const __grid_constant__ DevPlan Pin,
     const __grid_constant__ Ptrs src, const __grid_constant__ DevPlan Pout,
     const __grid_constant__ Ptrs dst, int64_t r0, int64_t r1, float* __restrict__ staged, uint32_t* status) {
