@@ -134,6 +134,16 @@ int smlrt_plan_create(const smlrt_view_t* views, int n_views, int n_sweep,
                       const int64_t* array_numel, int n_arrays,
                       smlrt_plan_t* out);
 int smlrt_plan_info(smlrt_plan_t plan, smlrt_plan_info_t* info);
+/* Element ranges [lo, hi) of a uniform 1-D-sweep plan's single array touched
+ * by sweep rows [r0, r1): one per column, sorted, overlapping/adjacent ones
+ * merged; `ranges` holds 2*max_ranges int64.  *exact = 1 when every element
+ * inside the ranges is touched (column stride 1 or dense row-major rows), so
+ * the ranges are also safe to copy back for a FROM plan.  Host-side chunking
+ * of host-resident arrays (copy a row block's bytes, launch on it). New in
+ * this runtime (no reference counterpart). SMLRT_E_UNSUPPORTED if the plan
+ * is not uniform / not 1-D or needs more than max_ranges ranges. */
+int smlrt_plan_row_ranges(smlrt_plan_t plan, int64_t r0, int64_t r1, int64_t* ranges, int32_t max_ranges,
+                          int32_t* n_ranges, int32_t* exact);
 int smlrt_plan_destroy(smlrt_plan_t plan);
 
 /*

@@ -81,6 +81,7 @@ SIGNATURES = {
     "smlrt_plan_create": (_I, [C.POINTER(View), _I, _I, C.POINTER(_I64), _I, C.POINTER(_I64), _I,
                                C.POINTER(_P)]),
     "smlrt_plan_info": (_I, [_P, C.POINTER(PlanInfo)]),
+    "smlrt_plan_row_ranges": (_I, [_P, _I64, _I64, C.POINTER(_I64), _I32, C.POINTER(_I32), C.POINTER(_I32)]),
     "smlrt_plan_destroy": (_I, [_P]),
     "smlrt_model_upload": (_I, [C.POINTER(Layer), _I, _I, _I, C.POINTER(_P)]),
     "smlrt_model_free": (_I, [_P]),
@@ -187,6 +188,18 @@ def plan_info(handle) -> dict:
     info = PlanInfo()
     _check(lib().smlrt_plan_info(handle, C.byref(info)))
     return {k: getattr(info, k) for k, _ in PlanInfo._fields_}
+
+
+def plan_row_ranges(handle, r0: int, r1: int, max_ranges: int = 16):
+    """[(lo, hi), ...] element ranges rows [r0, r1) touch, and whether they are
+    exact; None when the plan is not uniform 1-D or needs > max_ranges."""
+    buf = (_I64 * (2 * max_ranges))()
+    n, exact = _I32(0), _I32(0)
+    rc = lib().smlrt_plan_row_ranges(handle, r0, r1, buf, max_ranges, C.byref(n), C.byref(exact))
+    if rc == 10:  # SMLRT_E_UNSUPPORTED
+        return None
+    _check(rc)
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)], bool(exact.value)
 
 
 def plan_destroy(handle):

@@ -285,6 +285,33 @@ extern "C" int smlrt_plan_info(smlrt_plan_t p, smlrt_plan_info_t* info) {
   return SMLRT_OK;
 }
 
+extern "C" int smlrt_plan_row_ranges(smlrt_plan_t p, int64_t r0, int64_t r1, int64_t* ranges, int32_t max_ranges,
+                                     int32_t* n_ranges, int32_t* exact) {
+  if (!p || !ranges || !n_ranges || !exact) return fail(SMLRT_E_INVALID, "plan_row_ranges: null");
+  if (!p->uniform || p->n_sweep != 1) return fail(SMLRT_E_UNSUPPORTED, "plan_row_ranges: needs a uniform 1-D plan");
+  if (r0 < 0 || r1 > p->n_rows || r0 >= r1) return fail(SMLRT_E_INVALID, "plan_row_ranges: bad row range");
+  const int64_t s = p->ustride[0];
+  if (s < 1) return fail(SMLRT_E_UNSUPPORTED, "plan_row_ranges: non-positive row stride");
+  std::vector<std::pair<int64_t, int64_t>> iv;
+  iv.reserve(p->n_cols);
+  for (int c = 0; c < p->n_cols; ++c) iv.push_back({p->col_off[c] + r0 * s, p->col_off[c] + (r1 - 1) * s + 1});
+  std::sort(iv.begin(), iv.end());
+  int n = 0;
+  for (const auto& v : iv) {
+    if (n > 0 && v.first <= ranges[2 * n - 1]) {
+      ranges[2 * n - 1] = std::max(ranges[2 * n - 1], v.second);
+      continue;
+    }
+    if (n == max_ranges) return fail(SMLRT_E_UNSUPPORTED, "plan_row_ranges: more ranges than max_ranges");
+    ranges[2 * n] = v.first;
+    ranges[2 * n + 1] = v.second;
+    ++n;
+  }
+  *n_ranges = n;
+  *exact = (s == 1 || (p->dense_rows && s == p->n_cols)) ? 1 : 0;
+  return SMLRT_OK;
+}
+
 extern "C" int smlrt_plan_destroy(smlrt_plan_t p) {
   delete p;
   return SMLRT_OK;

@@ -509,9 +509,11 @@ class Runtime:
                              elapsed_map_to_ns=map_to, elapsed_map_from_ns=map_from,
                              elapsed_infer_ns=infer_ns)
 
-    # host-resident (pinned) row-major input and output: the row range is cut
-    # into chunks whose host->device copy, kernel and device->host copy run on
-    # three streams, so the PCIe transfers overlap the kernel and each other
+    # host-resident (pinned) input and output over uniform 1-D plans (AoS rows
+    # or SoA columns): the row range is cut into chunks whose host->device
+    # copies (the element ranges the chunk's rows touch, smlrt_plan_row_ranges),
+    # kernel and device->host copies run on three streams, so the PCIe
+    # transfers overlap the kernel and each other
     STREAM_MIN_ROWS = 1 << 18
     STREAM_CHUNK_ROWS = 1 << 17   # minimum rows per chunk; at most STREAM_CHUNKS chunks
     STREAM_CHUNKS = 16
@@ -521,8 +523,17 @@ class Runtime:
             return False
         if len(host_in) != 1 or len(host_out) != 1:
             return False
-        for m, plan in ((host_in[0], pin), (host_out[0], pout)):
-            if m.array.is_device or not m.array.data.is_pinned() or not _row_major(plan):
+        r0, r1 = _shard_rows(rows, self.shard)
+        if r1 <= r0:
+            return False
+        for m, plan, need_exact in ((host_in[0], pin, False), (host_out[0], pout, True)):
+            if m.array.is_device or not m.array.data.is_pinned() or len(plan.arrays) != 1:
+                return False
+            span = _native.plan_row_ranges(plan.handle, r0, r1)
+            if span is None or (need_exact and not span[1]):
+                return False
+            # gaps inside an input's ranges are copied too: allow at most 2x the touched elements
+            if sum(hi - lo for lo, hi in span[0]) > 2 * (r1 - r0) * plan.n_cols:
                 return False
         return True
 
@@ -537,7 +548,6 @@ class Runtime:
         status.zero_()
         hin, din = hin_map.array.data.view(-1), din_map.array.data.view(-1)
         hout, dout = hout_map.array.data.view(-1), dout_map.array.data.view(-1)
-        ci, co = pin.n_cols, pout.n_cols
         iptr, idt = pin.ptrs_and_dtypes()
         optr, odt = pout.ptrs_and_dtypes()
         up.wait_stream(cs)      # the mirrors may still be read/written by earlier work
@@ -546,13 +556,15 @@ class Runtime:
         for a in range(r0, r1, step):
             b = min(r1, a + step)
             with torch.cuda.stream(up):
-                din[a * ci:b * ci].copy_(hin[a * ci:b * ci], non_blocking=True)
+                for lo, hi in _native.plan_row_ranges(pin.handle, a, b)[0]:
+                    din[lo:hi].copy_(hin[lo:hi], non_blocking=True)
             cs.wait_stream(up)
             _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, a, b,
                                  _native.COMMIT_FUSED, None, cs.cuda_stream, status.data_ptr())
             down.wait_stream(cs)
             with torch.cuda.stream(down):
-                hout[a * co:b * co].copy_(dout[a * co:b * co], non_blocking=True)
+                for lo, hi in _native.plan_row_ranges(pout.handle, a, b)[0]:
+                    hout[lo:hi].copy_(dout[lo:hi], non_blocking=True)
         cs.wait_stream(down)
         bad = int(status.item())  # synchronises the stream
         infer_ns = _ns_since(t0)
@@ -594,16 +606,6 @@ def _flat_plan(groups, direction):
                                  (strides[-1],) + v.strides[v.n_sweep:], 1))
         flat.append(fv)
     return build_plan(flat, direction)
-
-
-def _row_major(plan: Plan) -> bool:
-    """True when plan row r touches exactly elements [r*n_cols, (r+1)*n_cols)
-    of the plan's single array (so a row range is one contiguous byte range)."""
-    if len(plan.arrays) != 1:
-        return False
-    info = _native.plan_info(plan.handle)
-    return bool(info["dense_rows"]) and info["row_pitch"] == plan.n_cols and \
-        plan.n_rows * plan.n_cols == plan.arrays[0].data.numel()
 
 
 def _covers(plan: Plan, array: ArrayBuffer) -> bool:

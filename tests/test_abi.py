@@ -83,3 +83,29 @@ def test_rows_limit_and_invalid_args():
     h = C.c_void_p()
     rc = lib.smlrt_plan_create(None, 0, 1, None, 0, None, 0, C.byref(h))
     assert rc == 9 and b"empty" in lib.smlrt_last_error()
+
+
+def test_plan_row_ranges():
+    """smlrt_plan_row_ranges: the element ranges a row block touches (the
+    chunked host path copies exactly these)."""
+    # AoS rows: one merged, exact range
+    p = plan("f: [k, 0:5] = ([k, 0:5])", [(0, 1000)], (1000, 5), "to")
+    assert _native.plan_row_ranges(p.handle, 10, 20) == ([(50, 100)], True)
+    # SoA columns: one exact range per feature
+    p = plan("f: [k, 0:6] = ([0:6, k])", [(0, 1000)], (6, 1000), "to")
+    rr, exact = _native.plan_row_ranges(p.handle, 100, 300)
+    assert exact and rr == [(c * 1000 + 100, c * 1000 + 300) for c in range(6)]
+    # SoA with a sub-slice of the sweep (offset base)
+    p = plan("f: [k, 0:2] = ([0:2, k])", [(5, 900)], (2, 1000), "to")
+    assert _native.plan_row_ranges(p.handle, 0, 10) == ([(5, 15), (1005, 1015)], True)
+    # strided columns of AoS records: merged span with gaps -> not exact
+    p = plan("f: [k, 0:2] = ([k, 0], [k, 3])", [(0, 1000)], (1000, 5), "to")
+    assert _native.plan_row_ranges(p.handle, 2, 4) == ([(10, 19)], False)
+    # too many ranges, or a 2-D sweep: unsupported -> None
+    p = plan("f: [k, 0:6] = ([0:6, k])", [(0, 1000)], (6, 1000), "to")
+    assert _native.plan_row_ranges(p.handle, 0, 10, max_ranges=4) is None
+    p = plan("f: [i, j, 0:5] = ([i-1, j], [i+1, j], [i, j-1:j+2])", [(1, 3), (1, 3)], (4, 4), "to")
+    assert _native.plan_row_ranges(p.handle, 0, 2) is None
+    p = plan("f: [k, 0:5] = ([k, 0:5])", [(0, 10)], (10, 5), "to")
+    with pytest.raises(ValueError):
+        _native.plan_row_ranges(p.handle, 5, 11)

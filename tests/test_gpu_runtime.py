@@ -245,7 +245,7 @@ def test_status_word_resets_between_calls(cuda, tmp_path, jdir):
                 rt.invoke_region(hb)
 
 
-@pytest.mark.parametrize("config,shard", [("bonds", None), ("bonds", (1, 3)), ("options", None)])
+@pytest.mark.parametrize("config,shard", [("bonds", None), ("bonds", (1, 3)), ("options", None), ("minibude", None), ("minibude", (0, 2))])
 def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, shard):
     """Pinned host input/output with row-major plans take the chunked
     three-stream path (H2D / kernel / D2H overlapped); results are bitwise
