@@ -14,6 +14,8 @@
 // The C4 ParticleFilter config (conv 8x8/8 1->8, relu, maxpool 2, 512->128
 // relu, 128->2) runs as front kernel + two tiled dense layers + scatter.
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
 
 #include <cstring>
 
@@ -294,7 +296,15 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
 // 128, one column block): the layer's activations stay in shared memory and
 // the next dense layer (out2 <= 4 units, e.g. C4's 128 -> 2) runs in the
 // same CTA, one ordered dot product per (row, unit).
-constexpr int PR = 32, PJ = 128, PK = 32;
+#ifndef SMLRT_PF_TC
+#define SMLRT_PF_TC 8
+#endif
+// TC = output columns per thread: 4 (32 rows x 128 columns per CTA) or 8 (64
+// rows: three LDS.128 per 32 packed FP instructions instead of two per 16);
+// with TC = 8 a thread's columns are two groups of four, [4 tj, +4) and
+// [64 + 4 tj, +4), so each group's float4 reads are contiguous across threads
+constexpr int PJ = 128, PK = 32, TC = SMLRT_PF_TC;
+constexpr int PR = 4 * (256 / (PJ / TC));
 
 template <bool FUSE2>
 __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict__ x, int64_t rows, int in, int out,
@@ -302,15 +312,22 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
                                                          int act, float* __restrict__ y, uint32_t* status,
                                                          const float* __restrict__ W2, const float* __restrict__ b2,
                                                          int out2, int act2, uint64_t one) {
-  __shared__ __align__(16) float xs[PK][PR + 4];
-  __shared__ __align__(16) float wsh[PK][PJ + 4];
-  __shared__ float hs[FUSE2 ? PR : 1][FUSE2 ? PJ + 1 : 1];
-  const int tr = threadIdx.x >> 5, tj = threadIdx.x & 31;  // rows 4 tr .. +3, columns 4 tj .. +3
+  constexpr int CG = PJ / TC, NG = TC / 4;  // column groups per CTA, float4 groups per thread
+  // hs (the fused tail's activations) reuses the K tiles' space after the K loop
+  constexpr int XB = PK * (PR + 4), WB = PK * (PJ + 4), HB = FUSE2 ? PR * (PJ + 1) : 1;
+  __shared__ __align__(16) float smem[XB + WB > HB ? XB + WB : HB];
+  auto xs = reinterpret_cast<float(*)[PR + 4]>(smem);
+  auto wsh = reinterpret_cast<float(*)[PJ + 4]>(smem + XB);
+  auto hs = reinterpret_cast<float(*)[FUSE2 ? PJ + 1 : 1]>(smem);
+  const int tr = threadIdx.x / CG, tj = threadIdx.x % CG;  // rows 4 tr .. +3
   const int64_t row0 = (int64_t)blockIdx.x * PR;
   const int j0 = blockIdx.y * PJ;
-  uint64_t acc[4][2];
+  auto col_of = [&](int g, int c) { return g * (PJ / NG) + 4 * tj + c; };  // group g, column c < 4
+  uint64_t acc[4][TC / 2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0ull;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int p = 0; p < TC / 2; ++p) acc[i][p] = 0ull;
   // the next K tile is fetched into registers while the current one is consumed
   constexpr int NX = PR * PK / 256, NW = PJ * PK / 256;
   float px[NX], pw[NW];
@@ -345,14 +362,19 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
     if (k0 + PK < in) fetch(k0 + PK);
     for (int k = 0; k < kn; ++k) {
       const float4 xv = *reinterpret_cast<const float4*>(&xs[k][tr * 4]);
-      const float4 wv = *reinterpret_cast<const float4*>(&wsh[k][tj * 4]);
-      const uint64_t w01 = cpk2(wv.x, wv.y), w23 = cpk2(wv.z, wv.w);
+      uint64_t w[TC / 2];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const float4 wv = *reinterpret_cast<const float4*>(&wsh[k][col_of(g, 0)]);
+        w[2 * g] = cpk2(wv.x, wv.y);
+        w[2 * g + 1] = cpk2(wv.z, wv.w);
+      }
       const float xr[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint64_t xx = cpk2(xr[i], xr[i]);
-        acc[i][0] = cadd2(acc[i][0], cmul2(xx, w01), one);
-        acc[i][1] = cadd2(acc[i][1], cmul2(xx, w23), one);
+#pragma unroll
+        for (int p = 0; p < TC / 2; ++p) acc[i][p] = cadd2(acc[i][p], cmul2(xx, w[p]), one);
       }
     }
     __syncthreads();
@@ -363,12 +385,12 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
     const int rl = tr * 4 + i;
     const int64_t r = row0 + rl;
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < TC / 2; ++p) {
       float v[2];
       cupk2(acc[i][p], v[0], v[1]);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int cl = tj * 4 + 2 * p + e, c = j0 + cl;
+        const int cl = col_of(p / 2, 2 * (p % 2) + e), c = j0 + cl;
         if (c < out) {
           const float hv = act_exact(__fadd_rn(v[e], __ldg(b + c)), act);
           if constexpr (FUSE2) {
@@ -532,30 +554,85 @@ int infer_cnn_dense(const smlrt_model_s& m, const float* x, int64_t rows, float*
   return rc;
 }
 
+namespace {
+// side stream per device for the conv front of the overlapped CNN region
+cudaStream_t front_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t st[64] = {};
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) st[dev] = nullptr;
+  return st[dev];
+}
+}  // namespace
+
+// Rows are processed in chunks of <= 16384 on the caller's stream.
+// Experiment (SMLRT_CNN_CHUNKS=k > 1, off by default): k chunks alternating
+// between two feature buffers, the conv front (HBM-bound) of chunk c+1 on a
+// side stream while the dense tail (FP32-bound) of chunk c runs on the
+// caller's stream, ordered by events (front c waits for the tail of c-2,
+// which read the same buffer).  Measured on C4 (16,384 windows): 1 / 2 / 3 / 4
+// chunks -> 0.330 / 0.397 / 0.416 / 0.443 ms -- the conv grid fills every SM,
+// so the kernels barely co-run and the smaller dense grids lose more.
 int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                       int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                       int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   if (!in.uniform) return fail(SMLRT_E_UNSUPPORTED, "CNN region needs a single-array input map");
+  static const int n_chunks = [] {
+    const char* e = std::getenv("SMLRT_CNN_CHUNKS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 1;
+  }();
   const int64_t rows = r1 - r0;
-  const int64_t ch = std::min<int64_t>(rows, 16384);
+  if (rows <= 0) return SMLRT_OK;
+  // >= 4096 rows per chunk keeps the dense tail's grid >= 64 CTAs
+  const int64_t ch = n_chunks > 1
+                         ? std::min<int64_t>(16384, std::max<int64_t>(4096, (rows + n_chunks - 1) / n_chunks))
+                         : std::min<int64_t>(16384, rows);
+  const int nbuf = n_chunks > 1 && rows > ch ? 2 : 1;
   size_t per = 1;  // widest activation after the conv front
   for (int l = 1; l < m.n_layers; ++l) per = std::max(per, (size_t)m.layers[l].out);
-  float *buf;
-  SMLRT_CUDA(cudaMallocAsync(&buf, (per * 3 + m.out_features) * ch * 4, s));
-  float* f = buf;
-  float* t0 = f + per * ch;
-  float* t1 = t0 + per * ch;
-  float* yo = t1 + per * ch;
+  const size_t slot = per * 3 + m.out_features;  // f, t0, t1, y per row
+  float* buf;
+  SMLRT_CUDA(cudaMallocAsync(&buf, slot * ch * 4 * nbuf, s));
+  int dev = 0;
+  SMLRT_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s2 = nbuf > 1 ? front_stream(dev) : nullptr;
+  cudaEvent_t ev[5] = {};  // [0] start, [1..2] front done per buffer, [3..4] tail done per buffer
+  if (s2) {
+    for (auto& e : ev) SMLRT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SMLRT_CUDA(cudaEventRecord(ev[0], s));
+    SMLRT_CUDA(cudaStreamWaitEvent(s2, ev[0], 0));
+  }
   int rc = SMLRT_OK;
-  for (int64_t r = r0; r < r1 && !rc; r += ch) {
+  int c = 0;
+  for (int64_t r = r0; r < r1 && !rc; r += ch, ++c) {
     const int64_t n = std::min(ch, r1 - r);
+    const int b = c % nbuf;
+    float* f = buf + slot * ch * b;
+    float* t0 = f + per * ch;
+    float* t1 = t0 + per * ch;
+    float* yo = t1 + per * ch;
+    cudaStream_t fs = s2 ? s2 : s;
+    if (s2 && c >= 2) SMLRT_CUDA(cudaStreamWaitEvent(s2, ev[3 + b], 0));
     int ow, nl;
-    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, s);
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, fs);
     if (rc) break;
+    if (s2) {
+      SMLRT_CUDA(cudaEventRecord(ev[1 + b], s2));
+      SMLRT_CUDA(cudaStreamWaitEvent(s, ev[1 + b], 0));
+    }
     float* ydst = staged ? staged + (r - r0) * m.out_features : yo;
     rc = dense_tail(m, nl, f, n, ydst, t0, t1, s, status);
     if (rc) break;
     if (!staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
+    if (s2) SMLRT_CUDA(cudaEventRecord(ev[3 + b], s));
+  }
+  if (s2) {
+    // the caller's stream owns the buffer again only after the side stream's last work
+    cudaEventRecord(ev[0], s2);
+    cudaStreamWaitEvent(s, ev[0], 0);
+    for (auto& e : ev) cudaEventDestroy(e);
   }
   cudaFreeAsync(buf, s);
   (void)n_in;
