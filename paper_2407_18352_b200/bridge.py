@@ -349,9 +349,12 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and _native.loaded():
-            _native.plan_destroy(h)
-            self.handle = None
+        try:  # at interpreter exit the module globals may already be gone
+            if h is not None and _native.loaded():
+                _native.plan_destroy(h)
+                self.handle = None
+        except Exception:
+            pass
 
 
 def build_plan(view_groups: Sequence[Sequence[MemoryView]], direction: str) -> Plan:

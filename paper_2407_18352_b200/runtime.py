@@ -514,12 +514,14 @@ class Runtime:
     # copies (the element ranges the chunk's rows touch, smlrt_plan_row_ranges),
     # kernel and device->host copies run on three streams, so the PCIe
     # transfers overlap the kernel and each other
-    STREAM_MIN_ROWS = 1 << 18
-    STREAM_CHUNK_ROWS = 1 << 17   # minimum rows per chunk; at most STREAM_CHUNKS chunks
+    # (below ~64 MB the per-chunk host overhead outweighs the overlap: options
+    # 20 MB, 0.64 ms staged whole vs 0.74 ms in 8 chunks)
+    STREAM_MIN_BYTES = 64 << 20
+    STREAM_CHUNK_BYTES = 16 << 20  # minimum input bytes per chunk; at most STREAM_CHUNKS chunks
     STREAM_CHUNKS = 16
 
     def _streamable(self, desc, host_in, host_out, pin, pout, rows) -> bool:
-        if self.time_kernels or self.commit != "fused" or rows < self.STREAM_MIN_ROWS or desc.inout_maps:
+        if self.time_kernels or self.commit != "fused" or desc.inout_maps:
             return False
         if len(host_in) != 1 or len(host_out) != 1:
             return False
@@ -535,7 +537,8 @@ class Runtime:
             # gaps inside an input's ranges are copied too: allow at most 2x the touched elements
             if sum(hi - lo for lo, hi in span[0]) > 2 * (r1 - r0) * plan.n_cols:
                 return False
-        return True
+        in_bytes = (r1 - r0) * pin.n_cols * host_in[0].array.data.element_size()
+        return in_bytes >= self.STREAM_MIN_BYTES
 
     def _run_streamed(self, st, hin_map, din_map, hout_map, dout_map, pin, pout, rows, handle, map_to):
         t0 = time.perf_counter_ns()
@@ -552,7 +555,8 @@ class Runtime:
         optr, odt = pout.ptrs_and_dtypes()
         up.wait_stream(cs)      # the mirrors may still be read/written by earlier work
         down.wait_stream(cs)
-        step = max(self.STREAM_CHUNK_ROWS, -(-(r1 - r0) // self.STREAM_CHUNKS))
+        row_bytes = pin.n_cols * hin.element_size()
+        step = max(-(-self.STREAM_CHUNK_BYTES // row_bytes), -(-(r1 - r0) // self.STREAM_CHUNKS))
         for a in range(r0, r1, step):
             b = min(r1, a + step)
             with torch.cuda.stream(up):

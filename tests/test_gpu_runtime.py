@@ -245,19 +245,28 @@ def test_status_word_resets_between_calls(cuda, tmp_path, jdir):
                 rt.invoke_region(hb)
 
 
-@pytest.mark.parametrize("config,shard", [("bonds", None), ("bonds", (1, 3)), ("options", None), ("minibude", None), ("minibude", (0, 2))])
-def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, shard):
-    """Pinned host input/output with row-major plans take the chunked
-    three-stream path (H2D / kernel / D2H overlapped); results are bitwise
-    those of the device-resident call, including a ragged last chunk."""
+def _small_chunks(rt):
+    # exercise the chunked path at test sizes: no size floor, ~1 MB chunks
+    rt.STREAM_MIN_BYTES = 0
+    rt.STREAM_CHUNK_BYTES = 1 << 20
+    return rt
+
+
+@pytest.mark.parametrize("config,n,shard", [("bonds", 312345, None), ("bonds", 312345, (1, 3)),
+                                            ("options", 312345, None), ("minibude", 312345, None),
+                                            ("minibude", 312345, (0, 2)), ("particlefilter", 601, None)])
+def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, n, shard):
+    """Pinned host input/output over uniform 1-D plans (AoS rows, SoA columns,
+    2-D windows) take the chunked three-stream path (H2D / kernel / D2H
+    overlapped); results are bitwise those of the device-resident call,
+    including a ragged last chunk."""
     from paper_2407_18352_b200 import workloads
-    n = 20 * sm.Runtime.STREAM_CHUNK_ROWS + 12345
     dev_wl = workloads.make(config, n)
     dev_wl.to_device()
     host_wl = workloads.make(config, n)
     host_wl.to_device(pinned_host=True)
     sm.save_model(dev_wl.model, tmp_path / "m")
-    with sm.Runtime(shard=shard) as rt:
+    with _small_chunks(sm.Runtime(shard=shard)) as rt:
         rt.invoke_region(rt.register_region(dev_wl.descriptor(str(tmp_path / "m"))))
         hd = host_wl.descriptor(str(tmp_path / "m"), name="host")
         plans_before = len(rt._plans)
@@ -270,15 +279,27 @@ def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, shard):
     assert np.array_equal(got, want)
 
 
+def test_chunked_host_path_size_floor(cuda, tmp_path):
+    """Below STREAM_MIN_BYTES the host buffers are staged whole (per-chunk
+    host overhead would outweigh the overlap)."""
+    from paper_2407_18352_b200 import workloads
+    wl = workloads.make("options", 100000)
+    wl.to_device(pinned_host=True)
+    sm.save_model(wl.model, tmp_path / "m")
+    with sm.Runtime() as rt:
+        rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "m"))))
+        assert rt._side is None
+
+
 def test_chunked_host_path_nonfinite(cuda, tmp_path):
     from paper_2407_18352_b200 import workloads
-    n = sm.Runtime.STREAM_MIN_ROWS + 7
+    n = 100007
     wl = workloads.make("bonds", n)
     wl.to_device(pinned_host=True)
     fi, fo, ti, to = wl.functors()
     wl.buffers[ti.array].data[-16:] = float("inf")  # last row of the last chunk
     sm.save_model(wl.model, tmp_path / "m")
-    with sm.Runtime() as rt:
+    with _small_chunks(sm.Runtime()) as rt:
         h = rt.register_region(wl.descriptor(str(tmp_path / "m")))
         with pytest.raises(NonFiniteOutputError):
             rt.invoke_region(h)
