@@ -68,7 +68,7 @@ constexpr int MMA2W = SMLRT_MMA2W;
 template <bool PAIR>
 constexpr int ss_threads() { return PAIR ? NTHREADS : NTHREADS + 32 * MMA2W; }
 #ifndef SMLRT_LDEPTH
-#define SMLRT_LDEPTH 2
+#define SMLRT_LDEPTH 1
 #endif
 constexpr int LDEPTH = SMLRT_LDEPTH;  // X tiles of global loads in flight per loader thread
 #ifndef SMLRT_L2DUAL
@@ -552,9 +552,11 @@ __global__ void __launch_bounds__(ss_threads<PAIR>(), 1)
     const uint32_t xbase = smem_u32(smem + L::OFF_X);
     if (a.x_fast != nullptr) {
       // tile = 2048 contiguous floats: thread t moves float4 #(t + 128 i), i < 4.
-      // Loads run LDEPTH tiles ahead in registers: with one tile in flight the
-      // loader had 8 KB outstanding per SM, ~0.9 TB/s at HBM latency, which
-      // capped the whole kernel (the MMA warp waited on X tiles).
+      // Loads run LDEPTH tiles ahead in registers (the next tile's loads are
+      // issued as soon as the current one is stored).  A first loader that
+      // issued them only after the XEMPTY wait capped the kernel at ~0.9 TB/s;
+      // with the split MMA issuers one tile ahead is enough and the fastest
+      // (LDEPTH 1 / 2 / 3: 0.966 / 1.005 / 1.008 ms).
       float4 buf[LDEPTH][4];
       auto load_tile = [&](int it, float4(&v)[4]) {
         const int64_t row0 = a.r0 + sc.tile(it) * BM;
