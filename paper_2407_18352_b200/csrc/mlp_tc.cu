@@ -159,6 +159,15 @@ __device__ __forceinline__ uint64_t add2f(uint64_t a, uint64_t b) {
   return r;
 }
 
+__device__ __forceinline__ uint64_t fma2f(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+#ifndef SMLRT_EPI2_PACKED
+#define SMLRT_EPI2_PACKED 1
+#endif
+
 struct Ptrs8 {
   const void* p[8];
   int32_t dt[8];
@@ -387,6 +396,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
     if (q == 0 && lane == 0) TR(6, it);
     tc_fence_after();
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};  // packed-pair partial sums (SMLRT_EPI2_PACKED)
 #if SMLRT_LDX64
     if constexpr (!PAIR && !DA && H2 % 64 == 0) {
       // 64 columns per TMEM request, half the wait points of the x32 loop
@@ -399,6 +409,25 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
           tc_fence_before();
           mbar_arrive(bar + L::B_L2EMPTY + b);
         }
+#if SMLRT_EPI2_PACKED
+        if constexpr (ACT != SMLRT_TANH) {
+          // packed pairs: add.f32x2 (b2), two max.NaN (relu), fma.f32x2 (w3):
+          // 2 instructions per hidden unit instead of 3
+#pragma unroll
+          for (int e = 0; e < 64; e += 2) {
+            const uint64_t bb = *reinterpret_cast<const uint64_t*>(a.b2 + c2 * 64 + e);
+            const uint64_t ww = *reinterpret_cast<const uint64_t*>(a.w3 + c2 * 64 + e);
+            uint64_t h = add2f((uint64_t)v[e] | ((uint64_t)v[e + 1] << 32), bb);
+            if constexpr (ACT == SMLRT_RELU) {
+              float lo, hi;
+              asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(h));
+              asm("mov.b64 %0, {%1, %2};" : "=l"(h) : "f"(relu_nan(lo)), "f"(relu_nan(hi)));
+            }
+            acc2[(e >> 1) & 3] = fma2f(h, ww, acc2[(e >> 1) & 3]);
+          }
+          continue;
+        }
+#endif
 #pragma unroll
         for (int e = 0; e < 64; e += 4) {
           const float4 ww = *reinterpret_cast<const float4*>(a.w3 + c2 * 64 + e);
@@ -445,6 +474,12 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
         acc[((e >> 2) & 1) * 4 + 2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2])), ww.z, acc[((e >> 2) & 1) * 4 + 2]);
         acc[((e >> 2) & 1) * 4 + 3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3])), ww.w, acc[((e >> 2) & 1) * 4 + 3]);
       }
+    }
+    for (int p = 0; p < 4; ++p) {
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc2[p]));
+      acc[2 * p] += lo;
+      acc[2 * p + 1] += hi;
     }
     const float y = act_f(((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + b3,
                           a.act3);
