@@ -96,6 +96,36 @@ struct GemmLay {
   static_assert(2 * BN <= 512 && BN % 16 == 0 && BN <= 256, "BN");
 };
 
+#ifndef SMLRT_GEMM_EPI_PACKED
+#define SMLRT_GEMM_EPI_PACKED 1
+#endif
+// packed f32x2 helpers for the EPI_DOT epilogue (bias add, relu, dot with w_next)
+__device__ __forceinline__ uint64_t gpk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t gadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t gfma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+template <int ACT>
+__device__ __forceinline__ uint64_t gact2(uint64_t h) {
+  if constexpr (ACT == SMLRT_RELU) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(h));
+    return gpk2(act_g<ACT>(lo), act_g<ACT>(hi));
+  } else {
+    return h;
+  }
+}
+
 template <int ACT, int BN, int EPI>
 __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, uint64_t* tempty, int n_my,
                                               int n_tiles_n, const GemmArgs& g, const float* bias_s,
@@ -111,6 +141,7 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
     tc_fence_after();
     const int64_t m = (int64_t)mb * GBM + r;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};  // packed partial sums (SMLRT_GEMM_EPI_PACKED)
     // 32 columns at a time; with BN a multiple of 64 each TMEM request
     // fetches 64 columns (half the wait points)
     auto consume = [&](const uint32_t* v, int c0) {
@@ -129,6 +160,22 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
           for (int j = 0; j < 4; ++j) o[j] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
         }
       } else {
+#if SMLRT_GEMM_EPI_PACKED
+        if constexpr (ACT != SMLRT_TANH) {
+          // add.f32x2 + relu + fma.f32x2 per pair, bias / w_next as LDS.128
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(bias_s + c0 + e);
+            const float4 ww = *reinterpret_cast<const float4*>(wn_s + c0 + e);
+            const uint64_t h0 = gact2<ACT>(gadd2(gpk2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), gpk2(bb.x, bb.y)));
+            const uint64_t h1 =
+                gact2<ACT>(gadd2(gpk2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])), gpk2(bb.z, bb.w)));
+            acc2[(e >> 1) & 3] = gfma2(h0, gpk2(ww.x, ww.y), acc2[(e >> 1) & 3]);
+            acc2[((e >> 1) + 1) & 3] = gfma2(h1, gpk2(ww.z, ww.w), acc2[((e >> 1) + 1) & 3]);
+          }
+          return;
+        }
+#endif
 #pragma unroll
         for (int e = 0; e < 32; ++e)
           acc[e & 7] = fmaf(act_g<ACT>(__uint_as_float(v[e]) + bias_s[c0 + e]), wn_s[c0 + e], acc[e & 7]);
@@ -161,6 +208,12 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
       }
     }
     if constexpr (EPI == EPI_DOT) {
+      for (int p = 0; p < 4; ++p) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc2[p]));
+        acc[2 * p] += lo;
+        acc[2 * p + 1] += hi;
+      }
       float y = ((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7])) + g.b_next;
       if (g.act_next == SMLRT_RELU) y = act_g<SMLRT_RELU>(y);
       else if (g.act_next == SMLRT_TANH) y = tanhf(y);
@@ -487,6 +540,20 @@ __device__ __forceinline__ void l12_epilogue(uint8_t* smem, uint64_t* bar, uint3
         for (int e4 = 0; e4 < 4; ++e4) {
           const float4 bb = ld_shared_f4(b2s + (c * 16 + 4 * e4) * 4);
           const uint32_t* vv = v + cc * 16 + 4 * e4;
+#if SMLRT_GEMM_EPI_PACKED
+          if constexpr (ACT2 != SMLRT_TANH) {
+            // add.f32x2 + one cvt(.relu).bf16x2 per pair: 2 instructions instead of 5
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const uint64_t hsum = gadd2(gpk2(__uint_as_float(vv[2 * u]), __uint_as_float(vv[2 * u + 1])),
+                                          gpk2(u ? bb.z : bb.x, u ? bb.w : bb.y));
+              float lo, hi;
+              asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(hsum));
+              p[2 * e4 + u] = ACT2 == SMLRT_RELU ? pack_relu_bf16(lo, hi) : pack_bf16(lo, hi);
+            }
+            continue;
+          }
+#endif
           p[2 * e4] = pack_bf16(act_g<ACT2>(__uint_as_float(vv[0]) + bb.x), act_g<ACT2>(__uint_as_float(vv[1]) + bb.y));
           p[2 * e4 + 1] =
               pack_bf16(act_g<ACT2>(__uint_as_float(vv[2]) + bb.z), act_g<ACT2>(__uint_as_float(vv[3]) + bb.w));
