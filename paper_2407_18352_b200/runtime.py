@@ -470,7 +470,13 @@ class Runtime:
         t0 = time.perf_counter_ns()
         iptr, idt = pin.ptrs_and_dtypes()
         optr, odt = pout.ptrs_and_dtypes()
-        flags = _native.COMMIT_CHECKED if self.commit == "checked" else _native.COMMIT_FUSED
+        # an output array sharing storage with an input array (inout maps, or
+        # in/out maps over one buffer): outputs are staged and scattered after
+        # every row has been gathered -- the reference's gather-all / infer /
+        # scatter order (runtime.py:315-357) -- instead of written from the
+        # fused epilogue while other rows may still be reading
+        staged = self.commit == "checked" or _shares_storage(pin, pout)
+        flags = _native.COMMIT_CHECKED if staged else _native.COMMIT_FUSED
         # device-resident outputs: status reset, launch, status read-back and
         # the stream sync happen inside one native call (SMLRT_SYNC_STATUS)
         # (kernel timing wants the events around the launches alone: old path)
@@ -527,6 +533,8 @@ class Runtime:
             return False
         r0, r1 = _shard_rows(rows, self.shard)
         if r1 <= r0:
+            return False
+        if _shares_storage(pin, pout):
             return False
         for m, plan, need_exact in ((host_in[0], pin, False), (host_out[0], pout, True)):
             if m.array.is_device or not m.array.data.is_pinned() or len(plan.arrays) != 1:
@@ -610,6 +618,21 @@ def _flat_plan(groups, direction):
                                  (strides[-1],) + v.strides[v.n_sweep:], 1))
         flat.append(fv)
     return build_plan(flat, direction)
+
+
+def _shares_storage(pin: Plan, pout: Plan) -> bool:
+    """True when any array the out plan writes overlaps (in device memory) an
+    array the in plan reads."""
+    def span(a):
+        t = a.data
+        lo = t.data_ptr()
+        return lo, lo + t.numel() * t.element_size()
+    ins = [span(a) for a in pin.arrays]
+    for a in pout.arrays:
+        lo, hi = span(a)
+        if any(lo < ihi and ilo < hi for ilo, ihi in ins):
+            return True
+    return False
 
 
 def _covers(plan: Plan, array: ArrayBuffer) -> bool:
