@@ -216,6 +216,12 @@ int smlrt_tc_selftest(int K, int N, const float* A, const float* B, float* D);
 /* Same with A staged in TMEM by tcgen05.st (the TS operand path). */
 int smlrt_tc_selftest_ts(int K, int N, const float* A, const float* B, float* D);
 
+/* Diagnostic: FP32 CUDA-core peak of the current device in flop/s for an
+ * instruction mix: 0 = FFMA, 1 = FMUL + FADD (no contraction), 2 = packed
+ * mul.rn.f32x2 + fma.rn.f32x2(p, 1, acc) -- the exact path's ordered
+ * multiply-then-add on f32x2 pairs.  The bench's fp32 roofline denominator. */
+int smlrt_fp32_peak(int32_t mode, double* flops_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,7 @@ SIGNATURES = {
     "smlrt_collect_wait": (_I, [_P]),
     "smlrt_tc_selftest": (_I, [_I, _I, _P, _P, _P]),
     "smlrt_tc_selftest_ts": (_I, [_I, _I, _P, _P, _P]),
+    "smlrt_fp32_peak": (_I, [_I32, C.POINTER(C.c_double)]),
 }
 
 _lib = None
@@ -297,3 +298,11 @@ def tc_selftest(A, B, tmem_a: bool = False):
     fn = lib().smlrt_tc_selftest_ts if tmem_a else lib().smlrt_tc_selftest
     _check(fn(A.shape[1], B.shape[0], A.ctypes.data, B.ctypes.data, D.ctypes.data))
     return D
+
+
+def fp32_peak(mode: int) -> float:
+    """Measured FP32 flop/s of the current device: 0 FFMA, 1 FMUL+FADD,
+    2 packed f32x2 mul then fma(p, 1, acc) (the exact kernels' mix)."""
+    v = C.c_double()
+    _check(lib().smlrt_fp32_peak(mode, C.byref(v)))
+    return float(v.value)

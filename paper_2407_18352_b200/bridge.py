@@ -335,8 +335,9 @@ class Plan:
     width; `n_rows` the flattened sweep size.
     """
 
-    def __init__(self, handle, arrays, n_rows, n_cols, sweep, direction):
+    def __init__(self, handle, arrays, n_rows, n_cols, sweep, direction, views=()):
         self.handle = handle
+        self.views = list(views)  # [(array index, MemoryView)]
         self.arrays = arrays
         self.n_rows = n_rows
         self.n_cols = n_cols
@@ -378,7 +379,7 @@ def build_plan(view_groups: Sequence[Sequence[MemoryView]], direction: str) -> P
             flat.append((index[key], v))
     handle, n_rows, n_cols = _native.plan_create(
         flat, sweep, direction, [a.data.numel() for a in arrays])
-    return Plan(handle, arrays, n_rows, n_cols, sweep, direction)
+    return Plan(handle, arrays, n_rows, n_cols, sweep, direction, flat)
 
 
 def _views_for(functor: FunctorDecl, target: MapTarget, array: ArrayBuffer):

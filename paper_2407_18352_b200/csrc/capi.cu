@@ -18,15 +18,18 @@ int device_tables(smlrt_plan_t p, DevPlan* d, const int32_t* dtypes, int n) {
   return SMLRT_OK;
 }
 
-// Keep the device's stream-ordered pool from returning memory at every
-// synchronisation, so per-call scratch is a pool hit after the first call.
+// Keep up to kPoolKeep bytes of the device's stream-ordered pool across
+// synchronisations, so per-call scratch is a pool hit after the first call;
+// larger one-off scratch (e.g. a checked commit's staged output) goes back
+// to the driver at the next synchronisation instead of staying reserved.
+constexpr uint64_t kPoolKeep = 1ull << 30;
 void warm_pool() {
   static int done_mask = 0;
   int d = 0;
   if (cudaGetDevice(&d) != cudaSuccess || (done_mask & (1 << d))) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
+    uint64_t keep = kPoolKeep;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   done_mask |= 1 << d;

@@ -383,6 +383,7 @@ constexpr int L12_H1MAX = 1024;
 
 template <int NH>
 struct L12Lay {
+  static constexpr int SA = L12_SA;
   static constexpr int A_BYTES = GBM * 64 * 2;
   static constexpr int B_BYTES = 256 * 64 * 2;
   static constexpr int OFF_A = 0;
@@ -432,10 +433,9 @@ __device__ __forceinline__ uint32_t act_pack2(uint64_t v) {
 // the tile for k pairs [8 cq, 8 cq + 8) of each 64-wide chunk: every
 // broadcast weight load (LDS.128) serves two rows, halving the producer's
 // share of the SMEM port the tensor core reads its operands through.
-template <int ACT1, int F>
-__device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n_my, const L12Args& a,
+template <int ACT1, int F, class L, class Args>
+__device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n_my, const Args& a,
                                              const DevPlan& Pin, int tid) {
-  using L = L12Lay<1>;  // A ring / W1 offsets do not depend on NH
   const int KB = a.H1 / 64;
   const int rq = tid & 63, cq = tid >> 6;
   const uint32_t w1s = smem_u32(smem + L::OFF_W1);  // explicit ld.shared (a generic load stalls on long scoreboard)
@@ -498,7 +498,7 @@ __device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n
       }
       fence_async_smem();
       mbar_arrive(bar + L::AFULL + s);
-      if (++s == L12_SA) {
+      if (++s == L::SA) {
         s = 0;
         ph ^= 1;
       }
@@ -668,11 +668,376 @@ __global__ void __launch_bounds__(l12_threads<NH>(), 1)
   } else {
     const int t = threadIdx.x - 32 * (2 + 4 * NH);
     if (a.act1 == SMLRT_RELU)
-      l12_producer<SMLRT_RELU, F>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_RELU, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t);
     else if (a.act1 == SMLRT_TANH)
-      l12_producer<SMLRT_TANH, F>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_TANH, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t);
     else
-      l12_producer<SMLRT_IDENTITY, F>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_IDENTITY, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+// ------------------------------------- fused layers 1-4 (C3, no HBM round trip)
+// The whole 6-1024-512-256-1 forward pass of a 128-row tile on one SM:
+//   layer 1  CUDA cores (producer warps, as in l12_fused_kernel) -> A1 ring
+//   layer 2  tcgen05, N = 512 as two 256-column TMEM regions R1 | R2, K = H1
+//            streamed in 64-wide A1 chunks against TMA W2 boxes [256 x 32]
+//   layer 3  the epilogue drains R1 then R2 (+b2, act, bf16) into a 4-slot
+//            ring of 64-wide K chunks (A3, SW128); tcgen05 multiplies them
+//            against TMA W3 boxes into R1 (free once drained): N = H3 = 256
+//   layer 4  the epilogue drains R1 (+b3, act, . w4, +b4, act) and scatters
+//            through the out plan (or stages for a checked commit)
+// so layer 2's [rows x 512] activations never leave the SM (the two-kernel
+// chain wrote and re-read 1 KB per row of HBM).  Per tile the tensor pipe
+// runs layer 2 (16,384 cycles at N = 256) then layer 3 (4,096); it waits
+// only for the R1 drain between them and the layer-4 drain before the next
+// tile's R1 writes.
+//
+// warp 0: TMA (W2 / W3 boxes)   warp 1: MMA issuer (warp-uniform, elect)
+// warps 2-9: epilogue, 2 per TMEM lane quarter (column halves)
+// warps 10-17: layer-1 producers (thread = two rows x 8 k pairs)
+constexpr int W4_EPI = 8, W4_PW = 8;
+constexpr int W4_THREADS = 32 * (2 + W4_EPI + W4_PW);
+struct W4Lay {
+  static constexpr int SA = 3;              // A1 ring (128 x 64 bf16, SW128)
+  static constexpr int SB = 4;              // B ring (W2 / W3 boxes, 256 x 32 bf16, SW64)
+  static constexpr int A_BYTES = GBM * 64 * 2;
+  static constexpr int B_BYTES = 256 * 32 * 2;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + SA * A_BYTES;
+  static constexpr int OFF_A3 = OFF_B + SB * B_BYTES;  // 4 slots, same layout as A1
+  static constexpr int OFF_W1 = OFF_A3 + 4 * A_BYTES;
+  static constexpr int OFF_B2 = OFF_W1 + L12_H1MAX / 2 * 64;
+  static constexpr int OFF_B3 = OFF_B2 + 512 * 4;
+  static constexpr int OFF_W4 = OFF_B3 + 256 * 4;
+  static constexpr int OFF_RED = OFF_W4 + 256 * 4;     // 128 partial dot products
+  static constexpr int OFF_BAR = OFF_RED + 128 * 4;
+  enum { AFULL = 0, AEMPTY = SA, BFULL = 2 * SA, BEMPTY = BFULL + SB, TFULL = BEMPTY + SB, R1FREE, R2FREE,
+         A3FULL, A3EMPTY = A3FULL + 4, L3FULL = A3EMPTY + 4, L3FREE, NBAR };
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
+  static_assert(ALLOC <= 232448, "shared memory budget");
+};
+
+struct W4Args {
+  int M, H1, F;
+  int act1, act2, act3, act4;
+  int64_t r0;               // sweep row of tile row 0
+  const float* w1p;         // layer-1 pair table (see l12_producer)
+  const float* b2;          // [512]
+  const float* b3;          // [256]
+  const float* w4;          // [256]
+  float b4;
+  const void* src;          // in-plan's array
+  int src_dt;
+  float* staged;            // checked commit: staged[row - r_stage0]
+  int64_t r_stage0;
+  uint32_t* status;
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int ACT>
+__device__ __forceinline__ uint64_t w4_act2(uint64_t h) {
+  if constexpr (ACT == SMLRT_TANH) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(h));
+    return gpk2(tanhf(lo), tanhf(hi));
+  } else {
+    return gact2<ACT>(h);
+  }
+}
+
+// drain 64 accumulator columns of this thread's row (+bias, act, bf16) into
+// one A3 chunk (SW128 K-major, row r)
+template <int ACT>
+__device__ __forceinline__ void w4_drain_chunk(uint32_t taddr, uint32_t bias_s, uint32_t dst, int r) {
+  uint32_t v[64];
+  tmem_ld64(taddr, v);
+  tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 8j .. 8j+7
+    uint32_t p[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 2; ++e2) {
+      const float4 bb = ld_shared_f4(bias_s + (8 * j + 4 * e2) * 4);
+      const uint32_t* vv = v + 8 * j + 4 * e2;
+      if constexpr (ACT != SMLRT_TANH) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint64_t hsum = gadd2(gpk2(__uint_as_float(vv[2 * u]), __uint_as_float(vv[2 * u + 1])),
+                                      gpk2(u ? bb.z : bb.x, u ? bb.w : bb.y));
+          float lo, hi;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(hsum));
+          p[2 * e2 + u] = ACT == SMLRT_RELU ? pack_relu_bf16(lo, hi) : pack_bf16(lo, hi);
+        }
+      } else {
+        p[2 * e2] = pack_bf16(tanhf(__uint_as_float(vv[0]) + bb.x), tanhf(__uint_as_float(vv[1]) + bb.y));
+        p[2 * e2 + 1] = pack_bf16(tanhf(__uint_as_float(vv[2]) + bb.z), tanhf(__uint_as_float(vv[3]) + bb.w));
+      }
+    }
+    st_shared_v4(dst + r * 128 + ((j ^ (r & 7)) << 4), p[0], p[1], p[2], p[3]);
+  }
+}
+
+template <int ACT2, int ACT3>
+__device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, const W4Args& a,
+                                            const DevPlan& Pout, const OutPtrs& dst, int q, int half, int lane) {
+  using L = W4Lay;
+  const int r = q * 32 + lane;
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  const uint32_t b2s = smem_u32(smem + L::OFF_B2), b3s = smem_u32(smem + L::OFF_B3), w4s = smem_u32(smem + L::OFF_W4);
+  const uint32_t a3 = smem_u32(smem + L::OFF_A3);
+  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);
+  for (int i = 0; i < n_my; ++i) {
+    const int64_t m = (int64_t)(blockIdx.x + i * gridDim.x) * GBM + r;
+    mbar_wait_sleep(bar + L::TFULL, i & 1);
+    tc_fence_after();
+    // layer-2 activations: R1 -> A3 chunks 0-3 (this half: 2 of them), then R2 -> chunks 4-7
+#pragma unroll 1
+    for (int reg = 0; reg < 2; ++reg) {
+#pragma unroll 1
+      for (int cc = 0; cc < 2; ++cc) {
+        const int slot = half * 2 + cc;                 // chunk c = 4 reg + slot
+        mbar_wait(bar + L::A3EMPTY + slot, reg ^ 1);    // slot use 2i + reg waits for use 2i + reg - 1
+        w4_drain_chunk<ACT2>(tbase + lane_off + reg * 256 + slot * 64, b2s + (reg * 256 + slot * 64) * 4,
+                             a3 + slot * L::A_BYTES, r);
+        fence_async_smem();
+        mbar_arrive(bar + L::A3FULL + slot);
+      }
+      tc_fence_before();
+      mbar_arrive(bar + (reg ? L::R2FREE : L::R1FREE));
+    }
+    // layer 3 accumulator (R1) -> +b3, act, . w4 over this half's 128 columns
+    mbar_wait_sleep(bar + L::L3FULL, i & 1);
+    tc_fence_after();
+    uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll 1
+    for (int c4 = 0; c4 < 2; ++c4) {
+      const int c0 = half * 128 + c4 * 64;
+      uint32_t v[64];
+      tmem_ld64(tbase + lane_off + c0, v);
+      tmem_wait_ld();
+      if (c4 == 1) {
+        tc_fence_before();
+        mbar_arrive(bar + L::L3FREE);
+      }
+#pragma unroll
+      for (int e = 0; e < 64; e += 4) {
+        const float4 bb = ld_shared_f4(b3s + (c0 + e) * 4);
+        const float4 ww = ld_shared_f4(w4s + (c0 + e) * 4);
+        const uint64_t h0 = w4_act2<ACT3>(gadd2(gpk2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), gpk2(bb.x, bb.y)));
+        const uint64_t h1 = w4_act2<ACT3>(gadd2(gpk2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])), gpk2(bb.z, bb.w)));
+        acc2[(e >> 1) & 3] = gfma2(h0, gpk2(ww.x, ww.y), acc2[(e >> 1) & 3]);
+        acc2[((e >> 1) + 1) & 3] = gfma2(h1, gpk2(ww.z, ww.w), acc2[((e >> 1) + 1) & 3]);
+      }
+    }
+    float part = 0.f;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc2[p]));
+      part += lo + hi;
+    }
+    if (half == 1) red[r] = part;
+    named_sync(1 + q, 64);
+    if (half == 0) {
+      float y = part + red[r] + a.b4;
+      if (a.act4 == SMLRT_RELU) y = act_g<SMLRT_RELU>(y);
+      else if (a.act4 == SMLRT_TANH) y = tanhf(y);
+      bool bad = false;
+      if (m < a.M) {
+        const int64_t row = a.r0 + m;
+        bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
+        if (a.staged != nullptr) {
+          a.staged[row - a.r_stage0] = y;
+        } else {
+          int64_t addr;
+          int arr;
+          if (Pout.uniform) {
+            addr = Pout.col_off0 + row_offset_uniform(Pout, (uint32_t)row);
+            arr = Pout.uarray;
+          } else {
+            uint32_t idx[SMLRT_MAX_SWEEP];
+            unravel(Pout, (uint32_t)row, idx);
+            addr = col_address(Pout, 0, idx);
+            arr = __ldg(Pout.col_arr);
+          }
+          if (dst.dt[arr] == SMLRT_F32)
+            reinterpret_cast<float*>(dst.p[arr])[addr] = y;
+          else
+            reinterpret_cast<double*>(dst.p[arr])[addr] = (double)y;
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+    }
+  }
+}
+
+template <int F>
+__global__ void __launch_bounds__(W4_THREADS, 1)
+    w4_fused_kernel(const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
+                    const __grid_constant__ W4Args a, const __grid_constant__ DevPlan Pin,
+                    const __grid_constant__ DevPlan Pout, const __grid_constant__ OutPtrs dst) {
+  using L = W4Lay;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+  const int n_tiles = (a.M + GBM - 1) / GBM;
+  const int n_my = (int)blockIdx.x < n_tiles ? (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int KB = a.H1 / 64;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < L::SA; ++i) {
+      mbar_init(bar + L::AFULL + i, 32 * W4_PW);
+      mbar_init(bar + L::AEMPTY + i, 1);
+    }
+    for (int i = 0; i < L::SB; ++i) {
+      mbar_init(bar + L::BFULL + i, 1);
+      mbar_init(bar + L::BEMPTY + i, 1);
+    }
+    mbar_init(bar + L::TFULL, 1);
+    mbar_init(bar + L::R1FREE, 32 * W4_EPI);
+    mbar_init(bar + L::R2FREE, 32 * W4_EPI);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(bar + L::A3FULL + i, 128);
+      mbar_init(bar + L::A3EMPTY + i, 1);
+    }
+    mbar_init(bar + L::L3FULL, 1);
+    mbar_init(bar + L::L3FREE, 32 * W4_EPI);
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tw2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tw3)) : "memory");
+  }
+  {
+    const float4* g = reinterpret_cast<const float4*>(a.w1p);
+    float4* w = reinterpret_cast<float4*>(smem + L::OFF_W1);
+    for (int i = threadIdx.x; i < a.H1 / 2 * 4; i += W4_THREADS) w[i] = g[i];
+    float* b2s = reinterpret_cast<float*>(smem + L::OFF_B2);
+    for (int i = threadIdx.x; i < 512; i += W4_THREADS) b2s[i] = a.b2[i];
+    float* b3s = reinterpret_cast<float*>(smem + L::OFF_B3);
+    float* w4s = reinterpret_cast<float*>(smem + L::OFF_W4);
+    for (int i = threadIdx.x; i < 256; i += W4_THREADS) {
+      b3s[i] = a.b3[i];
+      w4s[i] = a.w4[i];
+    }
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0, ph = 0;
+      auto load = [&](const CUtensorMap* map, int k0, int n0) {
+        mbar_wait_sleep(bar + L::BEMPTY + s, ph ^ 1);
+        mbar_expect_tx(bar + L::BFULL + s, L::B_BYTES);
+        tma_load_2d(smem_u32(smem + L::OFF_B + s * L::B_BYTES), map, bar + L::BFULL + s, k0, n0);
+        if (++s == L::SB) {
+          s = 0;
+          ph ^= 1;
+        }
+      };
+      for (int i = 0; i < n_my; ++i) {
+        for (int kb = 0; kb < KB; ++kb)
+          for (int h = 0; h < 2; ++h)
+            for (int kh = 0; kh < 2; ++kh) load(&tw2, kb * 64 + kh * 32, h * 256);
+        for (int c = 0; c < 8; ++c)
+          for (int kh = 0; kh < 2; ++kh) load(&tw3, c * 64 + kh * 32, 0);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(GBM, 256);
+    const uint64_t a0 = smem_desc(smem_u32(smem + L::OFF_A), 1024, kSwizzle128);
+    const uint64_t a30 = smem_desc(smem_u32(smem + L::OFF_A3), 1024, kSwizzle128);
+    const uint64_t b0 = smem_desc(smem_u32(smem + L::OFF_B), 512, kSwizzle64);
+    int sa = 0, pa = 0, sb = 0, pb = 0;
+    for (int i = 0; i < n_my; ++i) {
+      // ---- layer 2: R1 | R2 += A1 chunk x W2 boxes
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(bar + L::AFULL + sa, pa);
+        if (kb == 0) {
+          mbar_wait(bar + L::L3FREE, (i & 1) ^ 1);  // previous tile's layer-3 result drained from R1
+          mbar_wait(bar + L::R2FREE, (i & 1) ^ 1);
+        }
+        tc_fence_after();
+        const uint64_t ad = a0 + ((sa * L::A_BYTES) >> 4);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h)
+#pragma unroll 1
+          for (int kh = 0; kh < 2; ++kh) {
+            mbar_wait(bar + L::BFULL + sb, pb);
+            tc_fence_after();
+            const uint64_t bd = b0 + ((sb * L::B_BYTES) >> 4);
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              mma_ss_elect(tbase + h * 256, ad + (kh * 2 + k) * 2, bd + k * 2, idesc, (kb | kh | k) != 0);
+            mma_commit_elect(bar + L::BEMPTY + sb);
+            if (++sb == L::SB) {
+              sb = 0;
+              pb ^= 1;
+            }
+          }
+        mma_commit_elect(bar + L::AEMPTY + sa);
+        if (++sa == L::SA) {
+          sa = 0;
+          pa ^= 1;
+        }
+      }
+      mma_commit_elect(bar + L::TFULL);
+      // ---- layer 3: R1 = A3 chunks x W3 boxes (R1 drained first)
+      mbar_wait(bar + L::R1FREE, i & 1);
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        const int slot = c & 3;
+        mbar_wait(bar + L::A3FULL + slot, c >> 2);
+        tc_fence_after();
+        const uint64_t ad = a30 + ((slot * L::A_BYTES) >> 4);
+#pragma unroll 1
+        for (int kh = 0; kh < 2; ++kh) {
+          mbar_wait(bar + L::BFULL + sb, pb);
+          tc_fence_after();
+          const uint64_t bd = b0 + ((sb * L::B_BYTES) >> 4);
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            mma_ss_elect(tbase, ad + (kh * 2 + k) * 2, bd + k * 2, idesc, (c | kh | k) != 0);
+          mma_commit_elect(bar + L::BEMPTY + sb);
+          if (++sb == L::SB) {
+            sb = 0;
+            pb ^= 1;
+          }
+        }
+        mma_commit_elect(bar + L::A3EMPTY + slot);
+      }
+      mma_commit_elect(bar + L::L3FULL);
+    }
+  } else if (warp < 2 + W4_EPI) {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    if (a.act2 == SMLRT_RELU && a.act3 == SMLRT_RELU)
+      w4_epilogue<SMLRT_RELU, SMLRT_RELU>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane);
+    else if (a.act2 == SMLRT_TANH && a.act3 == SMLRT_TANH)
+      w4_epilogue<SMLRT_TANH, SMLRT_TANH>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane);
+    else
+      w4_epilogue<SMLRT_IDENTITY, SMLRT_IDENTITY>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane);
+  } else {
+    const int t = threadIdx.x - 32 * (2 + W4_EPI);
+    if (a.act1 == SMLRT_RELU)
+      l12_producer<SMLRT_RELU, F, W4Lay>(smem, bar, n_my, a, Pin, t);
+    else if (a.act1 == SMLRT_TANH)
+      l12_producer<SMLRT_TANH, F, W4Lay>(smem, bar, n_my, a, Pin, t);
+    else
+      l12_producer<SMLRT_IDENTITY, F, W4Lay>(smem, bar, n_my, a, Pin, t);
   }
   tc_fence_before();
   __syncthreads();
@@ -1015,7 +1380,7 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                   bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : (bk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SMLRT_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return SMLRT_OK;
@@ -1213,10 +1578,72 @@ int l12_launch(const CUtensorMap& tb, const L12Args& a, const DevPlan& in, cudaS
   return SMLRT_OK;
 }
 
+// the fully fused kernel: l12 shapes with H2 = 512, H3 = 256 and one
+// activation for layers 2 and 3 (SMLRT_WIDE_W4=0 selects the two-kernel chain)
+bool w4_shape(const smlrt_model_s& m) {
+  static const int off = [] {
+    const char* e = std::getenv("SMLRT_WIDE_W4");
+    return e && std::atoi(e) == 0;
+  }();
+  return !off && l12_shape(m) && m.layers[1].out == 512 && m.layers[2].out == 256 &&
+         m.layers[1].act == m.layers[2].act;
+}
+
+template <int F>
+int w4_launch(const CUtensorMap& tw2, const CUtensorMap& tw3, const W4Args& a, const DevPlan& in, const DevPlan& out,
+              const OutPtrs& dst, cudaStream_t s) {
+  static int configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1 << dev))) {
+    SMLRT_CUDA(cudaFuncSetAttribute(w4_fused_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, W4Lay::ALLOC));
+    configured |= 1 << dev;
+  }
+  const int tiles = (a.M + GBM - 1) / GBM;
+  const int grid = std::max(1, std::min(tiles, sm_count()));
+  w4_fused_kernel<F><<<grid, W4_THREADS, W4Lay::ALLOC, s>>>(tw2, tw3, a, in, out, dst);
+  count_launch();
+  SMLRT_CUDA(cudaGetLastError());
+  return SMLRT_OK;
+}
+
 int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                        const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
                        int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   if (!in.uniform) return fail(SMLRT_E_UNSUPPORTED, "wide path needs a single-array input map");
+  if (w4_shape(m) && in.n_cols == m.in_features && m.in_features <= SMLRT_INLINE_COLS && !l12_disabled()) {
+    const int h1 = m.layers[0].out;
+    const __nv_bfloat16* W2 = reinterpret_cast<const __nv_bfloat16*>(m.tc_blob) + (size_t)h1 * 16;
+    const __nv_bfloat16* W3 = W2 + (size_t)512 * h1;
+    CUtensorMap tw2, tw3;
+    if (int rc = make_map(&tw2, W2, 512, h1, h1, 256, 32)) return rc;
+    if (int rc = make_map(&tw3, W3, 256, 512, 512, 256, 32)) return rc;
+    OutPtrs dst{};
+    for (int i = 0; i < n_out && i < 8; ++i) {
+      dst.p[i] = out_ptrs[i];
+      dst.dt[i] = out_dt[i];
+    }
+    W4Args a{};
+    a.M = (int)(r1 - r0);
+    a.H1 = h1;
+    a.F = m.in_features;
+    a.act1 = m.layers[0].act;
+    a.act2 = m.layers[1].act;
+    a.act3 = m.layers[2].act;
+    a.act4 = m.layers[3].act;
+    a.r0 = r0;
+    a.w1p = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(m.tc_blob) + wide_w1p_off(m));
+    a.b2 = m.layers[1].b;
+    a.b3 = m.layers[2].b;
+    a.w4 = m.layers[3].w;
+    a.b4 = m.host_params.back();
+    a.src = in_ptrs[in.uarray];
+    a.src_dt = in_dt[in.uarray];
+    a.staged = staged;
+    a.r_stage0 = r0;
+    a.status = status;
+    return m.in_features <= 6 ? w4_launch<6>(tw2, tw3, a, in, out, dst, s) : w4_launch<7>(tw2, tw3, a, in, out, dst, s);
+  }
   const int F = m.in_features, h1 = m.layers[0].out, h2 = m.layers[1].out, h3 = m.layers[2].out;
   const __nv_bfloat16* W1p = reinterpret_cast<const __nv_bfloat16*>(m.tc_blob);
   const __nv_bfloat16* W2 = W1p + (size_t)h1 * 16;

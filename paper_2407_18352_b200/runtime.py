@@ -194,6 +194,7 @@ class Runtime:
         self._plans: dict[str, tuple] = {}
         self._staging = _Staging()
         self._side = None  # (host->device, device->host) streams of the chunked host path
+        self._collect_side = None  # device->host stream of the collect snapshots
         self.precision = precision
         self.commit = commit
         self.shard = shard
@@ -366,9 +367,9 @@ class Runtime:
         return host, t
 
     def _side_stream(self):
-        s = getattr(self, "_side", None)
+        s = self._collect_side
         if s is None:
-            s = self._side = torch.cuda.Stream(self.device)
+            s = self._collect_side = torch.cuda.Stream(self.device)
         return s
 
     def _run_collect(self, desc, st) -> RegionOutcome:
@@ -454,13 +455,25 @@ class Runtime:
             raise ModelShapeMismatchError(
                 f"region {desc.name!r} scatters {out_counts} features, model emits {model.output_features}")
         handle = device_model(model, self.device, self.precision)
-        if self._streamable(desc, host_in, host_out, pin, pout, rows):
-            return self._run_streamed(st, host_in[0], in_maps[0], host_out[0], out_maps[0], pin, pout, rows,
+        chunks = self._stream_chunks(desc, host_in, host_out, pin, pout, rows)
+        if chunks is not None:
+            return self._run_streamed(st, host_in[0], in_maps[0], host_out[0], out_maps[0], pin, pout, chunks,
                                       handle, _ns_since(t0))
+        # an output array sharing storage with an input array (inout maps, or
+        # in/out maps over one buffer): outputs are staged and scattered after
+        # every row has been gathered -- the reference's gather-all / infer /
+        # scatter order (runtime.py:315-357) -- instead of written from the
+        # fused epilogue while other rows may still be reading
+        staged = self.commit == "checked" or _shares_storage(pin, pout)
         for m, d in zip(host_in, in_maps):
             self._staging.upload(m.array, d.array)
+        # a host output's device mirror is downloaded whole afterwards, so it
+        # must hold the host's values wherever this call may not write: skip
+        # the upload only when the scatter surely writes every element (no
+        # shard, and no checked/staged commit that writes nothing on error)
+        skip_ok = self.shard is None and not staged
         for m, d in zip(host_out, out_maps):
-            if not m.array.is_device and not _covers(pout, d.array):
+            if not m.array.is_device and not (skip_ok and _covers(pout, d.array)):
                 self._staging.upload(m.array, d.array)
         r0, r1 = _shard_rows(rows, self.shard)
         status = self._status_word()
@@ -470,12 +483,6 @@ class Runtime:
         t0 = time.perf_counter_ns()
         iptr, idt = pin.ptrs_and_dtypes()
         optr, odt = pout.ptrs_and_dtypes()
-        # an output array sharing storage with an input array (inout maps, or
-        # in/out maps over one buffer): outputs are staged and scattered after
-        # every row has been gathered -- the reference's gather-all / infer /
-        # scatter order (runtime.py:315-357) -- instead of written from the
-        # fused epilogue while other rows may still be reading
-        staged = self.commit == "checked" or _shares_storage(pin, pout)
         flags = _native.COMMIT_CHECKED if staged else _native.COMMIT_FUSED
         # device-resident outputs: status reset, launch, status read-back and
         # the stream sync happen inside one native call (SMLRT_SYNC_STATUS)
@@ -526,31 +533,45 @@ class Runtime:
     STREAM_CHUNK_BYTES = 16 << 20  # minimum input bytes per chunk; at most STREAM_CHUNKS chunks
     STREAM_CHUNKS = 16
 
-    def _streamable(self, desc, host_in, host_out, pin, pout, rows) -> bool:
+    def _stream_chunks(self, desc, host_in, host_out, pin, pout, rows):
+        """The chunk schedule of the chunked host path -- [(a, b, in_ranges,
+        out_ranges)] -- or None when the call does not qualify.  Every chunk's
+        element ranges are computed before anything is launched: a plan whose
+        whole-range intervals merge (e.g. SoA columns) may still need more
+        ranges per chunk than plan_row_ranges allows, and then the call takes
+        the whole-array path instead of failing half-way."""
         if self.time_kernels or self.commit != "fused" or desc.inout_maps:
-            return False
+            return None
         if len(host_in) != 1 or len(host_out) != 1:
-            return False
+            return None
         r0, r1 = _shard_rows(rows, self.shard)
         if r1 <= r0:
-            return False
+            return None
         if _shares_storage(pin, pout):
-            return False
-        for m, plan, need_exact in ((host_in[0], pin, False), (host_out[0], pout, True)):
+            return None
+        for m, plan in ((host_in[0], pin), (host_out[0], pout)):
             if m.array.is_device or not m.array.data.is_pinned() or len(plan.arrays) != 1:
-                return False
-            span = _native.plan_row_ranges(plan.handle, r0, r1)
-            if span is None or (need_exact and not span[1]):
-                return False
-            # gaps inside an input's ranges are copied too: allow at most 2x the touched elements
-            if sum(hi - lo for lo, hi in span[0]) > 2 * (r1 - r0) * plan.n_cols:
-                return False
+                return None
         in_bytes = (r1 - r0) * pin.n_cols * host_in[0].array.data.element_size()
-        return in_bytes >= self.STREAM_MIN_BYTES
+        if in_bytes < self.STREAM_MIN_BYTES:
+            return None
+        row_bytes = pin.n_cols * host_in[0].array.data.element_size()
+        step = max(-(-self.STREAM_CHUNK_BYTES // row_bytes), -(-(r1 - r0) // self.STREAM_CHUNKS))
+        chunks = []
+        for a in range(r0, r1, step):
+            b = min(r1, a + step)
+            ri = _native.plan_row_ranges(pin.handle, a, b)
+            ro = _native.plan_row_ranges(pout.handle, a, b)
+            if ri is None or ro is None or not ro[1]:
+                return None
+            # gaps inside an input's ranges are copied too: allow at most 2x the touched elements
+            if sum(hi - lo for lo, hi in ri[0]) > 2 * (b - a) * pin.n_cols:
+                return None
+            chunks.append((a, b, ri[0], ro[0]))
+        return chunks
 
-    def _run_streamed(self, st, hin_map, din_map, hout_map, dout_map, pin, pout, rows, handle, map_to):
+    def _run_streamed(self, st, hin_map, din_map, hout_map, dout_map, pin, pout, chunks, handle, map_to):
         t0 = time.perf_counter_ns()
-        r0, r1 = _shard_rows(rows, self.shard)
         cs = torch.cuda.current_stream(self.device)
         if self._side is None:
             self._side = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
@@ -563,19 +584,16 @@ class Runtime:
         optr, odt = pout.ptrs_and_dtypes()
         up.wait_stream(cs)      # the mirrors may still be read/written by earlier work
         down.wait_stream(cs)
-        row_bytes = pin.n_cols * hin.element_size()
-        step = max(-(-self.STREAM_CHUNK_BYTES // row_bytes), -(-(r1 - r0) // self.STREAM_CHUNKS))
-        for a in range(r0, r1, step):
-            b = min(r1, a + step)
+        for a, b, in_ranges, out_ranges in chunks:
             with torch.cuda.stream(up):
-                for lo, hi in _native.plan_row_ranges(pin.handle, a, b)[0]:
+                for lo, hi in in_ranges:
                     din[lo:hi].copy_(hin[lo:hi], non_blocking=True)
             cs.wait_stream(up)
             _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, a, b,
                                  _native.COMMIT_FUSED, None, cs.cuda_stream, status.data_ptr())
             down.wait_stream(cs)
             with torch.cuda.stream(down):
-                for lo, hi in _native.plan_row_ranges(pout.handle, a, b)[0]:
+                for lo, hi in out_ranges:
                     hout[lo:hi].copy_(dout[lo:hi], non_blocking=True)
         cs.wait_stream(down)
         bad = int(status.item())  # synchronises the stream
@@ -621,17 +639,70 @@ def _flat_plan(groups, direction):
 
 
 def _shares_storage(pin: Plan, pout: Plan) -> bool:
-    """True when any array the out plan writes overlaps (in device memory) an
-    array the in plan reads."""
+    """True when an element the out plan writes may be an element the in plan
+    reads (in device memory).  Arrays that do not overlap at all, or whose
+    touched address intervals do not overlap, are independent; over one
+    buffer, views whose sweep strides share a pitch P and whose touched
+    offsets mod P are disjoint (e.g. an AoS record's input fields and a
+    separate output field) are independent too.  Anything else counts as
+    shared (conservative: the call is staged)."""
     def span(a):
         t = a.data
         lo = t.data_ptr()
         return lo, lo + t.numel() * t.element_size()
-    ins = [span(a) for a in pin.arrays]
-    for a in pout.arrays:
-        lo, hi = span(a)
-        if any(lo < ihi and ilo < hi for ilo, ihi in ins):
-            return True
+
+    def touched(plan, k):
+        a = plan.arrays[k]
+        es = a.data.element_size()
+        base = a.data.data_ptr()
+        out = []
+        for idx, v in plan.views:
+            if idx != k:
+                continue
+            hi = v.base_offset + sum((n - 1) * st for n, st in zip(v.shape, v.strides))
+            out.append((v, base + v.base_offset * es, base + (hi + 1) * es))
+        return out
+
+    def residues(v, pitch, limit=4096):
+        feat_n, feat_s = v.shape[v.n_sweep:], v.strides[v.n_sweep:]
+        if int(np.prod(feat_n)) > limit:
+            return None
+        offs = {v.base_offset % pitch}
+        for n, st in zip(feat_n, feat_s):
+            offs = {(o + i * st) % pitch for o in offs for i in range(n)}
+        return offs
+
+    for ko, ao in enumerate(pout.arrays):
+        olo, ohi = span(ao)
+        for ki, ai in enumerate(pin.arrays):
+            ilo, ihi = span(ai)
+            if not (olo < ihi and ilo < ohi):
+                continue
+            tin, tout = touched(pin, ki), touched(pout, ko)
+            if not any(a0 < b1 and b0 < a1 for _, a0, a1 in tin for _, b0, b1 in tout):
+                continue
+            if ai.data.data_ptr() != ao.data.data_ptr() or ai.data.element_size() != ao.data.element_size():
+                return True
+            pitch = 0
+            for v, _, _ in tin + tout:
+                for n, st in zip(v.shape[: v.n_sweep], v.strides[: v.n_sweep]):
+                    if n > 1:
+                        pitch = int(np.gcd(pitch, st))
+            if pitch <= 1:
+                return True
+            rin, rout = set(), set()
+            for v, _, _ in tin:
+                r = residues(v, pitch)
+                if r is None:
+                    return True
+                rin |= r
+            for v, _, _ in tout:
+                r = residues(v, pitch)
+                if r is None:
+                    return True
+                rout |= r
+            if rin & rout:
+                return True
     return False
 
 
