@@ -433,9 +433,34 @@ __device__ __forceinline__ uint32_t act_pack2(uint64_t v) {
 // the tile for k pairs [8 cq, 8 cq + 8) of each 64-wide chunk: every
 // broadcast weight load (LDS.128) serves two rows, halving the producer's
 // share of the SMEM port the tensor core reads its operands through.
-template <int ACT1, int F, class L, class Args>
+// Tile rows of a persistent CTA: tile i of this CTA starts at row
+// (first + i * stride) * rows + off (a CTA pair: 256-row pair tiles, rank r
+// owning rows [128 r, 128 r + 128)).
+struct TileRows {
+  int first, stride, rows, off;
+  __device__ __forceinline__ int64_t row0(int i) const { return (int64_t)(first + i * stride) * rows + off; }
+};
+// AFULL arrival: 0 = every thread on the local barrier, 1 = one elected lane
+// per warp on the local barrier, 2 = one lane per warp on the pair leader's
+// (rank 0) barrier through the cluster window
+template <int ARR>
+__device__ __forceinline__ void producer_arrive(uint64_t* bar) {
+  if constexpr (ARR == 0) {
+    mbar_arrive(bar);
+  } else {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if constexpr (ARR == 1)
+        mbar_arrive(bar);
+      else
+        mbar_arrive_remote(mapa(bar, 0));
+    }
+  }
+}
+
+template <int ACT1, int F, class L, class Args, int ARR = 0>
 __device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n_my, const Args& a,
-                                             const DevPlan& Pin, int tid) {
+                                             const DevPlan& Pin, int tid, TileRows tr) {
   const int KB = a.H1 / 64;
   const int rq = tid & 63, cq = tid >> 6;
   const uint32_t w1s = smem_u32(smem + L::OFF_W1);  // explicit ld.shared (a generic load stalls on long scoreboard)
@@ -443,7 +468,7 @@ __device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n
   auto load_x = [&](int i, float (&x)[2][F]) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t m = (int64_t)(blockIdx.x + i * gridDim.x) * GBM + rq + 64 * h;
+      const int64_t m = tr.row0(i) + rq + 64 * h;
       const int64_t ro = m < a.M ? row_offset_uniform(Pin, (uint32_t)(a.r0 + m)) : 0;
 #pragma unroll
       for (int f = 0; f < F; ++f) {
@@ -497,7 +522,7 @@ __device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n
         }
       }
       fence_async_smem();
-      mbar_arrive(bar + L::AFULL + s);
+      producer_arrive<ARR>(bar + L::AFULL + s);
       if (++s == L::SA) {
         s = 0;
         ph ^= 1;
@@ -668,11 +693,11 @@ __global__ void __launch_bounds__(l12_threads<NH>(), 1)
   } else {
     const int t = threadIdx.x - 32 * (2 + 4 * NH);
     if (a.act1 == SMLRT_RELU)
-      l12_producer<SMLRT_RELU, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_RELU, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t, TileRows{(int)blockIdx.x, (int)gridDim.x, GBM, 0});
     else if (a.act1 == SMLRT_TANH)
-      l12_producer<SMLRT_TANH, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_TANH, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t, TileRows{(int)blockIdx.x, (int)gridDim.x, GBM, 0});
     else
-      l12_producer<SMLRT_IDENTITY, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_IDENTITY, F, L12Lay<1>>(smem, bar, n_my, a, Pin, t, TileRows{(int)blockIdx.x, (int)gridDim.x, GBM, 0});
   }
   tc_fence_before();
   __syncthreads();
@@ -703,11 +728,16 @@ __global__ void __launch_bounds__(l12_threads<NH>(), 1)
 // warps 10-17: layer-1 producers (thread = two rows x 8 k pairs)
 constexpr int W4_EPI = 8, W4_PW = 8;
 constexpr int W4_THREADS = 32 * (2 + W4_EPI + W4_PW);
+// NS = 2: CTA pair (cta_group::2).  Rank 0 issues M = 256 MMAs over both
+// CTAs' A1 / A3 rings and TMEM; every W box is split along N, each CTA
+// loading its 128-row half (half the L2 -> SMEM weight traffic per SM, and
+// twice the ring depth in the same shared memory).
+template <int NS>
 struct W4Lay {
-  static constexpr int SA = 3;              // A1 ring (128 x 64 bf16, SW128)
-  static constexpr int SB = 4;              // B ring (W2 / W3 boxes, 256 x 32 bf16, SW64)
+  static constexpr int SA = 3;                        // A1 ring (128 x 64 bf16, SW128)
+  static constexpr int SB = 4 * NS;                   // B ring (this CTA's part of a [256 x 32] box, SW64)
   static constexpr int A_BYTES = GBM * 64 * 2;
-  static constexpr int B_BYTES = 256 * 32 * 2;
+  static constexpr int B_BYTES = 256 / NS * 32 * 2;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + SA * A_BYTES;
   static constexpr int OFF_A3 = OFF_B + SB * B_BYTES;  // 4 slots, same layout as A1
@@ -717,7 +747,7 @@ struct W4Lay {
   static constexpr int OFF_W4 = OFF_B3 + 256 * 4;
   static constexpr int OFF_RED = OFF_W4 + 256 * 4;     // 128 partial dot products
   static constexpr int OFF_BAR = OFF_RED + 128 * 4;
-  enum { AFULL = 0, AEMPTY = SA, BFULL = 2 * SA, BEMPTY = BFULL + SB, TFULL = BEMPTY + SB, R1FREE, R2FREE,
+  enum { AFULL = 0, AEMPTY = SA, BFULL = 2 * SA, BEMPTY = BFULL + SB, TFULL = BEMPTY + SB, TFULL1, R1FREE, R2FREE,
          A3FULL, A3EMPTY = A3FULL + 4, L3FULL = A3EMPTY + 4, L3FREE, NBAR };
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
   static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
@@ -742,6 +772,52 @@ struct W4Args {
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// one arrival per warp on the MMA issuer's barrier (the pair leader's)
+template <int NS>
+__device__ __forceinline__ void warp_arrive_mma(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    if constexpr (NS == 2)
+      mbar_arrive_remote(mapa(bar, 0));
+    else
+      mbar_arrive(bar);
+  }
+}
+// waits of the MMA issuer (also on barriers the peer CTA arrives on): a
+// cta-scope acquire -- the cluster-scope form costs an L1 invalidate
+// (CCTL.IVALL) per wait, and the MMA issuer reads no global memory
+template <int NS>
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+}
+template <int NS>
+__device__ __forceinline__ void w4_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (NS == 2)
+    mma2_ss_elect(d, a, b, idesc, acc);
+  else
+    mma_ss_elect(d, a, b, idesc, acc);
+}
+template <int NS>
+__device__ __forceinline__ void w4_commit(uint64_t* bar) {
+  if constexpr (NS == 2)
+    mma2_commit_mc_elect(bar, 0x3);
+  else
+    mma_commit_elect(bar);
+}
+// this CTA's half of a W box; the bytes complete on the leader's BFULL
+template <int NS>
+__device__ __forceinline__ void w4_tma(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  if constexpr (NS == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mapa(bar, 0))
+        : "memory");
+  } else {
+    tma_load_2d(dst, map, bar, c0, c1);
+  }
 }
 
 template <int ACT>
@@ -787,22 +863,24 @@ __device__ __forceinline__ void w4_drain_chunk(uint32_t taddr, uint32_t bias_s, 
   }
 }
 
-template <int ACT2, int ACT3>
+template <int ACT2, int ACT3, int NS>
 __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, const W4Args& a,
-                                            const DevPlan& Pout, const OutPtrs& dst, int q, int half, int lane) {
-  using L = W4Lay;
+                                            const DevPlan& Pout, const OutPtrs& dst, int q, int half, int lane,
+                                            TileRows tr) {
+  using L = W4Lay<NS>;
   const int r = q * 32 + lane;
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
   const uint32_t b2s = smem_u32(smem + L::OFF_B2), b3s = smem_u32(smem + L::OFF_B3), w4s = smem_u32(smem + L::OFF_W4);
   const uint32_t a3 = smem_u32(smem + L::OFF_A3);
   float* red = reinterpret_cast<float*>(smem + L::OFF_RED);
   for (int i = 0; i < n_my; ++i) {
-    const int64_t m = (int64_t)(blockIdx.x + i * gridDim.x) * GBM + r;
-    mbar_wait_sleep(bar + L::TFULL, i & 1);
-    tc_fence_after();
-    // layer-2 activations: R1 -> A3 chunks 0-3 (this half: 2 of them), then R2 -> chunks 4-7
+    const int64_t m = tr.row0(i) + r;
+    // layer-2 activations: R1 -> A3 chunks 0-3 (this half: 2 of them), then R2 -> chunks 4-7;
+    // R1's last MMAs are issued before R2's (TFULL1), so its drain overlaps them
 #pragma unroll 1
     for (int reg = 0; reg < 2; ++reg) {
+      mbar_wait_sleep(bar + (reg ? L::TFULL : L::TFULL1), i & 1);
+      tc_fence_after();
 #pragma unroll 1
       for (int cc = 0; cc < 2; ++cc) {
         const int slot = half * 2 + cc;                 // chunk c = 4 reg + slot
@@ -810,10 +888,10 @@ __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32
         w4_drain_chunk<ACT2>(tbase + lane_off + reg * 256 + slot * 64, b2s + (reg * 256 + slot * 64) * 4,
                              a3 + slot * L::A_BYTES, r);
         fence_async_smem();
-        mbar_arrive(bar + L::A3FULL + slot);
+        warp_arrive_mma<NS>(bar + L::A3FULL + slot);
       }
       tc_fence_before();
-      mbar_arrive(bar + (reg ? L::R2FREE : L::R1FREE));
+      warp_arrive_mma<NS>(bar + (reg ? L::R2FREE : L::R1FREE));
     }
     // layer 3 accumulator (R1) -> +b3, act, . w4 over this half's 128 columns
     mbar_wait_sleep(bar + L::L3FULL, i & 1);
@@ -827,7 +905,7 @@ __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32
       tmem_wait_ld();
       if (c4 == 1) {
         tc_fence_before();
-        mbar_arrive(bar + L::L3FREE);
+        warp_arrive_mma<NS>(bar + L::L3FREE);
       }
 #pragma unroll
       for (int e = 0; e < 64; e += 4) {
@@ -881,24 +959,28 @@ __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32
   }
 }
 
-template <int F>
+template <int F, int NS>
 __global__ void __launch_bounds__(W4_THREADS, 1)
     w4_fused_kernel(const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
                     const __grid_constant__ W4Args a, const __grid_constant__ DevPlan Pin,
                     const __grid_constant__ DevPlan Pout, const __grid_constant__ OutPtrs dst) {
-  using L = W4Lay;
+  using L = W4Lay<NS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
-  const int n_tiles = (a.M + GBM - 1) / GBM;
-  const int n_my = (int)blockIdx.x < n_tiles ? (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int rank = NS == 2 ? (int)cluster_rank() : 0;
+  // tiles of GBM * NS rows; this CTA owns rows [rank * GBM, rank * GBM + GBM) of each
+  const int n_tiles = (a.M + GBM * NS - 1) / (GBM * NS);
+  const int unit = (int)blockIdx.x / NS, units = (int)gridDim.x / NS;
+  const int n_my = unit < n_tiles ? (n_tiles - unit + units - 1) / units : 0;
+  const TileRows tr{unit, units, GBM * NS, rank * GBM};
   const int KB = a.H1 / 64;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < L::SA; ++i) {
-      mbar_init(bar + L::AFULL + i, 32 * W4_PW);
+      mbar_init(bar + L::AFULL + i, W4_PW * NS);
       mbar_init(bar + L::AEMPTY + i, 1);
     }
     for (int i = 0; i < L::SB; ++i) {
@@ -906,14 +988,15 @@ __global__ void __launch_bounds__(W4_THREADS, 1)
       mbar_init(bar + L::BEMPTY + i, 1);
     }
     mbar_init(bar + L::TFULL, 1);
-    mbar_init(bar + L::R1FREE, 32 * W4_EPI);
-    mbar_init(bar + L::R2FREE, 32 * W4_EPI);
+    mbar_init(bar + L::TFULL1, 1);
+    mbar_init(bar + L::R1FREE, W4_EPI * NS);
+    mbar_init(bar + L::R2FREE, W4_EPI * NS);
     for (int i = 0; i < 4; ++i) {
-      mbar_init(bar + L::A3FULL + i, 128);
+      mbar_init(bar + L::A3FULL + i, 4 * NS);
       mbar_init(bar + L::A3EMPTY + i, 1);
     }
     mbar_init(bar + L::L3FULL, 1);
-    mbar_init(bar + L::L3FREE, 32 * W4_EPI);
+    mbar_init(bar + L::L3FREE, W4_EPI * NS);
     mbar_fence_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tw2)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tw3)) : "memory");
@@ -931,9 +1014,17 @@ __global__ void __launch_bounds__(W4_THREADS, 1)
       w4s[i] = a.w4[i];
     }
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) {
+    if constexpr (NS == 2)
+      tmem_alloc2(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (NS == 2)
+    cluster_sync();  // peer barriers initialised and TMEM allocated before any remote arrive / MMA
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
@@ -942,108 +1033,127 @@ __global__ void __launch_bounds__(W4_THREADS, 1)
       int s = 0, ph = 0;
       auto load = [&](const CUtensorMap* map, int k0, int n0) {
         mbar_wait_sleep(bar + L::BEMPTY + s, ph ^ 1);
-        mbar_expect_tx(bar + L::BFULL + s, L::B_BYTES);
-        tma_load_2d(smem_u32(smem + L::OFF_B + s * L::B_BYTES), map, bar + L::BFULL + s, k0, n0);
+        if (rank == 0) mbar_expect_tx(bar + L::BFULL + s, L::B_BYTES * NS);
+        w4_tma<NS>(smem_u32(smem + L::OFF_B + s * L::B_BYTES), map, bar + L::BFULL + s, k0, n0);
         if (++s == L::SB) {
           s = 0;
           ph ^= 1;
         }
       };
+      const int nh = rank * (256 / NS);  // this CTA's rows of each box
       for (int i = 0; i < n_my; ++i) {
         for (int kb = 0; kb < KB; ++kb)
-          for (int h = 0; h < 2; ++h)
-            for (int kh = 0; kh < 2; ++kh) load(&tw2, kb * 64 + kh * 32, h * 256);
+          for (int hh = 0; hh < 2; ++hh) {
+            const int h = kb == 0 ? 1 - hh : hh;  // the MMA issuer's region order
+            for (int kh = 0; kh < 2; ++kh) load(&tw2, kb * 64 + kh * 32, h * 256 + nh);
+          }
         for (int c = 0; c < 8; ++c)
-          for (int kh = 0; kh < 2; ++kh) load(&tw3, c * 64 + kh * 32, 0);
+          for (int kh = 0; kh < 2; ++kh) load(&tw3, c * 64 + kh * 32, nh);
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(GBM, 256);
-    const uint64_t a0 = smem_desc(smem_u32(smem + L::OFF_A), 1024, kSwizzle128);
-    const uint64_t a30 = smem_desc(smem_u32(smem + L::OFF_A3), 1024, kSwizzle128);
-    const uint64_t b0 = smem_desc(smem_u32(smem + L::OFF_B), 512, kSwizzle64);
-    int sa = 0, pa = 0, sb = 0, pb = 0;
-    for (int i = 0; i < n_my; ++i) {
-      // ---- layer 2: R1 | R2 += A1 chunk x W2 boxes
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(bar + L::AFULL + sa, pa);
-        if (kb == 0) {
-          mbar_wait(bar + L::L3FREE, (i & 1) ^ 1);  // previous tile's layer-3 result drained from R1
-          mbar_wait(bar + L::R2FREE, (i & 1) ^ 1);
-        }
-        tc_fence_after();
-        const uint64_t ad = a0 + ((sa * L::A_BYTES) >> 4);
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(GBM * NS, 256);
+      const uint64_t a0 = smem_desc(smem_u32(smem + L::OFF_A), 1024, kSwizzle128);
+      const uint64_t a30 = smem_desc(smem_u32(smem + L::OFF_A3), 1024, kSwizzle128);
+      const uint64_t b0 = smem_desc(smem_u32(smem + L::OFF_B), 512, kSwizzle64);
+      int sa = 0, pa = 0, sb = 0, pb = 0;
+      for (int i = 0; i < n_my; ++i) {
+        // ---- layer 2: R1 | R2 += A1 chunk x W2 boxes
+        // the first chunk goes to R2 first (drained during the previous
+        // tile's layer 3) while the layer-4 drain still reads R1; the last
+        // chunk finishes R1 first so its drain overlaps R2's last MMAs
+        for (int kb = 0; kb < KB; ++kb) {
+          mma_wait<NS>(bar + L::AFULL + sa, pa);
+          tc_fence_after();
+          const uint64_t ad = a0 + ((sa * L::A_BYTES) >> 4);
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h)
+          for (int hh = 0; hh < 2; ++hh) {
+            const int h = kb == 0 ? 1 - hh : hh;
+            if (kb == 0) {
+              mma_wait<NS>(bar + (h ? L::R2FREE : L::L3FREE), (i & 1) ^ 1);
+              tc_fence_after();
+            }
+#pragma unroll 1
+            for (int kh = 0; kh < 2; ++kh) {
+              mma_wait<NS>(bar + L::BFULL + sb, pb);
+              tc_fence_after();
+              const uint64_t bd = b0 + ((sb * L::B_BYTES) >> 4);
+#pragma unroll
+              for (int k = 0; k < 2; ++k)
+                w4_mma<NS>(tbase + h * 256, ad + (kh * 2 + k) * 2, bd + k * 2, idesc, (kb | kh | k) != 0);
+              w4_commit<NS>(bar + L::BEMPTY + sb);
+              if (++sb == L::SB) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+            if (kb == KB - 1 && h == 0) w4_commit<NS>(bar + L::TFULL1);
+          }
+          w4_commit<NS>(bar + L::AEMPTY + sa);
+          if (++sa == L::SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+        }
+        w4_commit<NS>(bar + L::TFULL);
+        // ---- layer 3: R1 = A3 chunks x W3 boxes (R1 drained first)
+        mma_wait<NS>(bar + L::R1FREE, i & 1);
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          const int slot = c & 3;
+          mma_wait<NS>(bar + L::A3FULL + slot, c >> 2);
+          tc_fence_after();
+          const uint64_t ad = a30 + ((slot * L::A_BYTES) >> 4);
 #pragma unroll 1
           for (int kh = 0; kh < 2; ++kh) {
-            mbar_wait(bar + L::BFULL + sb, pb);
+            mma_wait<NS>(bar + L::BFULL + sb, pb);
             tc_fence_after();
             const uint64_t bd = b0 + ((sb * L::B_BYTES) >> 4);
 #pragma unroll
             for (int k = 0; k < 2; ++k)
-              mma_ss_elect(tbase + h * 256, ad + (kh * 2 + k) * 2, bd + k * 2, idesc, (kb | kh | k) != 0);
-            mma_commit_elect(bar + L::BEMPTY + sb);
+              w4_mma<NS>(tbase, ad + (kh * 2 + k) * 2, bd + k * 2, idesc, (c | kh | k) != 0);
+            w4_commit<NS>(bar + L::BEMPTY + sb);
             if (++sb == L::SB) {
               sb = 0;
               pb ^= 1;
             }
           }
-        mma_commit_elect(bar + L::AEMPTY + sa);
-        if (++sa == L::SA) {
-          sa = 0;
-          pa ^= 1;
+          w4_commit<NS>(bar + L::A3EMPTY + slot);
         }
+        w4_commit<NS>(bar + L::L3FULL);
       }
-      mma_commit_elect(bar + L::TFULL);
-      // ---- layer 3: R1 = A3 chunks x W3 boxes (R1 drained first)
-      mbar_wait(bar + L::R1FREE, i & 1);
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        const int slot = c & 3;
-        mbar_wait(bar + L::A3FULL + slot, c >> 2);
-        tc_fence_after();
-        const uint64_t ad = a30 + ((slot * L::A_BYTES) >> 4);
-#pragma unroll 1
-        for (int kh = 0; kh < 2; ++kh) {
-          mbar_wait(bar + L::BFULL + sb, pb);
-          tc_fence_after();
-          const uint64_t bd = b0 + ((sb * L::B_BYTES) >> 4);
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-            mma_ss_elect(tbase, ad + (kh * 2 + k) * 2, bd + k * 2, idesc, (c | kh | k) != 0);
-          mma_commit_elect(bar + L::BEMPTY + sb);
-          if (++sb == L::SB) {
-            sb = 0;
-            pb ^= 1;
-          }
-        }
-        mma_commit_elect(bar + L::A3EMPTY + slot);
-      }
-      mma_commit_elect(bar + L::L3FULL);
     }
+    __syncwarp();
   } else if (warp < 2 + W4_EPI) {
     const int q = warp & 3, half = (warp - 2) >> 2;
     if (a.act2 == SMLRT_RELU && a.act3 == SMLRT_RELU)
-      w4_epilogue<SMLRT_RELU, SMLRT_RELU>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane);
+      w4_epilogue<SMLRT_RELU, SMLRT_RELU, NS>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane, tr);
     else if (a.act2 == SMLRT_TANH && a.act3 == SMLRT_TANH)
-      w4_epilogue<SMLRT_TANH, SMLRT_TANH>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane);
+      w4_epilogue<SMLRT_TANH, SMLRT_TANH, NS>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane, tr);
     else
-      w4_epilogue<SMLRT_IDENTITY, SMLRT_IDENTITY>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane);
+      w4_epilogue<SMLRT_IDENTITY, SMLRT_IDENTITY, NS>(smem, bar, tbase, n_my, a, Pout, dst, q, half, lane, tr);
   } else {
     const int t = threadIdx.x - 32 * (2 + W4_EPI);
+    constexpr int ARR = NS == 2 ? 2 : 1;
     if (a.act1 == SMLRT_RELU)
-      l12_producer<SMLRT_RELU, F, W4Lay>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_RELU, F, L, W4Args, ARR>(smem, bar, n_my, a, Pin, t, tr);
     else if (a.act1 == SMLRT_TANH)
-      l12_producer<SMLRT_TANH, F, W4Lay>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_TANH, F, L, W4Args, ARR>(smem, bar, n_my, a, Pin, t, tr);
     else
-      l12_producer<SMLRT_IDENTITY, F, W4Lay>(smem, bar, n_my, a, Pin, t);
+      l12_producer<SMLRT_IDENTITY, F, L, W4Args, ARR>(smem, bar, n_my, a, Pin, t, tr);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (NS == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    if constexpr (NS == 2)
+      tmem_dealloc2(tbase, 512);
+    else
+      tmem_dealloc(tbase, 512);
   }
 }
 
@@ -1589,19 +1699,48 @@ bool w4_shape(const smlrt_model_s& m) {
          m.layers[1].act == m.layers[2].act;
 }
 
-template <int F>
+// CTA pairs (cta_group::2: half of every W box per SM, half the L2 -> SMEM
+// weight traffic) by default; SMLRT_W4_PAIR=0 runs one CTA per 128-row tile.
+// C3 step, power-capped: pair 75.2 ms at ~1.72 GHz, single 78.6 ms at
+// ~1.61 GHz -- per clock they are even, the pair draws less power
+bool w4_pair() {
+  static const int v = [] {
+    const char* e = std::getenv("SMLRT_W4_PAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+template <int F, int NS>
 int w4_launch(const CUtensorMap& tw2, const CUtensorMap& tw3, const W4Args& a, const DevPlan& in, const DevPlan& out,
               const OutPtrs& dst, cudaStream_t s) {
+  using L = W4Lay<NS>;
   static int configured = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured & (1 << dev))) {
-    SMLRT_CUDA(cudaFuncSetAttribute(w4_fused_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, W4Lay::ALLOC));
+    SMLRT_CUDA(cudaFuncSetAttribute(w4_fused_kernel<F, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::ALLOC));
     configured |= 1 << dev;
   }
-  const int tiles = (a.M + GBM - 1) / GBM;
-  const int grid = std::max(1, std::min(tiles, sm_count()));
-  w4_fused_kernel<F><<<grid, W4_THREADS, W4Lay::ALLOC, s>>>(tw2, tw3, a, in, out, dst);
+  const int tiles = (a.M + GBM * NS - 1) / (GBM * NS);
+  const int grid = NS * std::max(1, std::min(tiles, sm_count() / NS));
+  if constexpr (NS == 1) {
+    w4_fused_kernel<F, 1><<<grid, W4_THREADS, L::ALLOC, s>>>(tw2, tw3, a, in, out, dst);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(W4_THREADS);
+    cfg.dynamicSmemBytes = L::ALLOC;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SMLRT_CUDA(cudaLaunchKernelEx(&cfg, w4_fused_kernel<F, 2>, tw2, tw3, a, in, out, dst));
+  }
   count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
@@ -1615,9 +1754,10 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
     const int h1 = m.layers[0].out;
     const __nv_bfloat16* W2 = reinterpret_cast<const __nv_bfloat16*>(m.tc_blob) + (size_t)h1 * 16;
     const __nv_bfloat16* W3 = W2 + (size_t)512 * h1;
+    const bool pair = w4_pair();
     CUtensorMap tw2, tw3;
-    if (int rc = make_map(&tw2, W2, 512, h1, h1, 256, 32)) return rc;
-    if (int rc = make_map(&tw3, W3, 256, 512, 512, 256, 32)) return rc;
+    if (int rc = make_map(&tw2, W2, 512, h1, h1, pair ? 128 : 256, 32)) return rc;
+    if (int rc = make_map(&tw3, W3, 256, 512, 512, pair ? 128 : 256, 32)) return rc;
     OutPtrs dst{};
     for (int i = 0; i < n_out && i < 8; ++i) {
       dst.p[i] = out_ptrs[i];
@@ -1642,7 +1782,11 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
     a.staged = staged;
     a.r_stage0 = r0;
     a.status = status;
-    return m.in_features <= 6 ? w4_launch<6>(tw2, tw3, a, in, out, dst, s) : w4_launch<7>(tw2, tw3, a, in, out, dst, s);
+    if (pair)
+      return m.in_features <= 6 ? w4_launch<6, 2>(tw2, tw3, a, in, out, dst, s)
+                                : w4_launch<7, 2>(tw2, tw3, a, in, out, dst, s);
+    return m.in_features <= 6 ? w4_launch<6, 1>(tw2, tw3, a, in, out, dst, s)
+                              : w4_launch<7, 1>(tw2, tw3, a, in, out, dst, s);
   }
   const int F = m.in_features, h1 = m.layers[0].out, h2 = m.layers[1].out, h3 = m.layers[2].out;
   const __nv_bfloat16* W1p = reinterpret_cast<const __nv_bfloat16*>(m.tc_blob);

@@ -68,9 +68,12 @@ def test_minibude_full_size_subsample(cuda, tmp_path):
     check_tol(got[idx], ref[:, 0].astype(np.float64))
 
 
-def test_minibude_tcgen05_layer1_variant(cuda, tmp_path):
-    """The opt-in tcgen05 layer-1 kernel (SMLRT_WIDE_L1=tc) meets the same
-    tolerances (run in a subprocess: the switch is read once per process)."""
+@pytest.mark.parametrize("env", [{"SMLRT_W4_PAIR": "0"}, {"SMLRT_WIDE_W4": "0"},
+                                 {"SMLRT_WIDE_W4": "0", "SMLRT_WIDE_L1": "tc"}])
+def test_minibude_kernel_variants(cuda, tmp_path, env):
+    """The single-CTA fused kernel (SMLRT_W4_PAIR=0), the two-kernel chain
+    (SMLRT_WIDE_W4=0) and its tcgen05 layer-1 variant meet the same
+    tolerances (subprocesses: the switches are read once per process)."""
     import os
     import subprocess
     import sys
@@ -84,6 +87,22 @@ def test_minibude_tcgen05_layer1_variant(cuda, tmp_path):
             "emu = t.emulate(wl.layers, x)[:, 0];"
             "assert np.max(np.abs(got - emu)) <= 2e-3 * max(1.0, np.abs(emu).max()); print('ok')")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "SMLRT_WIDE_L1": "tc"},
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("act", ["tanh", "identity"])
+def test_wide_fused_activations(cuda, tmp_path, act):
+    """Same shape, other hidden activations (the fused kernel's tanh / identity
+    instantiations) against the fp32 oracle."""
+    n = 9000
+    layers = workloads.init_weights([6, 1024, 512, 256, 1], act)
+    model = sm.Model(6, 1, [sm.DenseLayer(w, b, a) for w, b, a in layers], precision="bf16")
+    wl = workloads.make("minibude", n)
+    wl.layers, wl.model = layers, model
+    wl.to_device()
+    got = run(wl, tmp_path)
+    x = np.ascontiguousarray(wl.arrays["poses"].T)
+    ref, _ = c_oracle.mlp_f32(layers, x)
+    check_tol(got, ref[:, 0].astype(np.float64))
