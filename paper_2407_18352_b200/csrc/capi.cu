@@ -67,6 +67,7 @@ smlrt_model_s::~smlrt_model_s() {
     cudaFree(L.b);
   }
   cudaFree(tc_blob);
+  cudaFree(chain_blob);
   cudaSetDevice(prev);
 }
 
@@ -174,7 +175,7 @@ extern "C" int smlrt_model_path(smlrt_model_t m, int32_t n_in_cols, int32_t* pat
                          0, nullptr, true) == SMLRT_OK)
       *path = 3;
     else
-      *path = 0;
+      *path = chain_ok(*m) ? 5 : 0;
   } else if (launch_region_exact_fused(*m, dummy, nullptr, nullptr, 0, dummy, nullptr, nullptr, 0, 0,
                                        0, nullptr, 0, nullptr, true) == SMLRT_OK) {
     *path = 1;
@@ -336,7 +337,7 @@ static int region_launch(smlrt_plan_t pin, const void* const* in_ptrs, const int
                                      pout->n_arrays, r0, r1, staged, s, status, false);
     if (rc != SMLRT_OK && rc != SMLRT_E_UNSUPPORTED) return rc;
     if (rc == SMLRT_E_UNSUPPORTED && m->precision == SMLRT_BF16)
-      return fail(SMLRT_E_UNSUPPORTED, "no tcgen05 kernel for this model shape");
+      return rc;  // launch_region_chain's message: the model has non-dense or > 4096-wide layers
   }
   if (rc == SMLRT_E_UNSUPPORTED) {
     // unfused exact path: gather -> per-layer kernels -> scatter, chunked

@@ -172,6 +172,14 @@ struct smlrt_model_s {
   std::vector<float> host_params;  // packed [W0,b0,W1,b1,...] for the templated path
   void* tc_blob = nullptr;          // tcgen05 path: packed bf16 weights + f32 bias
   size_t tc_bytes = 0;
+  // generic tcgen05 layer chain (any dense model): per layer the bf16 weights
+  // [n_pad x k_pad] (K-major, zero padded) and f32 bias [n_pad] in chain_blob
+  struct ChainLayer {
+    int k_pad, n_pad, n, act;
+    size_t w_off, b_off;  // byte offsets in chain_blob
+  };
+  std::vector<ChainLayer> chain;
+  void* chain_blob = nullptr;
   ~smlrt_model_s();
 };
 
@@ -213,5 +221,11 @@ int wide_pack(smlrt_model_s& m);
 int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                        const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
                        int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
+// generic tcgen05 layer chain (gemm_tc.cu): any dense model, any plans
+bool chain_ok(const smlrt_model_s& m);
+int chain_pack(smlrt_model_s& m);
+int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
+                        int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
+                        int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 
 }  // namespace smlrt

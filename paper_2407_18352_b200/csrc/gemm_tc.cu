@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "simt_common.cuh"
 #include "tc_ptx.cuh"
 
 namespace smlrt {
@@ -31,7 +32,7 @@ using namespace ptx;
 
 constexpr int GBM = 128;
 constexpr int GTHREADS = 192;
-enum { EPI_BF16 = 0, EPI_DOT = 1 };
+enum { EPI_BF16 = 0, EPI_DOT = 1, EPI_F32 = 2 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -64,6 +65,9 @@ struct GemmArgs {
   // EPI_BF16
   __nv_bfloat16* out;      // [M][ldo]
   int64_t ldo;
+  // EPI_F32: act(acc + bias) as f32 for columns n < n_valid, row stride ldo
+  float* out_f32;
+  int n_valid;
   // EPI_DOT
   const float* w_next;     // [N]
   float b_next;
@@ -85,7 +89,7 @@ struct GemmLay {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int OFF_BIAS = STAGES * STAGE;
-  static constexpr int OFF_WN = OFF_BIAS + 1024 * 4;
+  static constexpr int OFF_WN = OFF_BIAS + 4096 * 4;
   static constexpr int OFF_BAR = OFF_WN + 256 * 4;
   static constexpr int N_BAR = 2 * STAGES + 4;
   static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
@@ -146,7 +150,22 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
     // fetches 64 columns (half the wait points)
     auto consume = [&](const uint32_t* v, int c0) {
       const int n0 = nb * BN + c0;
-      if constexpr (EPI == EPI_BF16) {
+      if constexpr (EPI == EPI_F32) {
+        bool bad = false;
+        if (m < g.M) {
+          float* o = g.out_f32 + m * g.ldo;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int n = n0 + e;
+            if (n < g.n_valid) {
+              const float y = act_g<ACT>(__uint_as_float(v[e]) + bias_s[n]);
+              bad |= (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
+              o[n] = y;
+            }
+          }
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(g.status, SMLRT_STATUS_NONFINITE);
+      } else if constexpr (EPI == EPI_BF16) {
         uint32_t p[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -282,7 +301,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
   }
-  for (int i = threadIdx.x; i < g.N && i < 1024; i += GTHREADS) bias_s[i] = g.bias[i];
+  for (int i = threadIdx.x; i < g.N && i < 4096; i += GTHREADS) bias_s[i] = g.bias[i];
   if (EPI == EPI_DOT)
     for (int i = threadIdx.x; i < g.N && i < 256; i += GTHREADS) wn_s[i] = g.w_next[i];
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512))));
@@ -440,6 +459,18 @@ struct TileRows {
   int first, stride, rows, off;
   __device__ __forceinline__ int64_t row0(int i) const { return (int64_t)(first + i * stride) * rows + off; }
 };
+// waits of the TMA and epilogue roles: plain try_wait polling by default
+// (SMLRT_W4_SLEEP=1: suspend-hinted try_wait)
+#ifndef SMLRT_W4_SLEEP
+#define SMLRT_W4_SLEEP 0
+#endif
+__device__ __forceinline__ void w4_wait(uint64_t* bar, uint32_t parity) {
+#if SMLRT_W4_SLEEP
+  mbar_wait_sleep(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 // AFULL arrival: 0 = every thread on the local barrier, 1 = one elected lane
 // per warp on the local barrier, 2 = one lane per warp on the pair leader's
 // (rank 0) barrier through the cluster window
@@ -495,7 +526,10 @@ __device__ __forceinline__ void l12_producer(uint8_t* smem, uint64_t* bar, int n
       }
     load_x(i + 1, xn);
     for (int kb = 0; kb < KB; ++kb) {
-      mbar_wait_sleep(bar + L::AEMPTY + s, ph ^ 1);
+      if constexpr (ARR == 0)
+        mbar_wait_sleep(bar + L::AEMPTY + s, ph ^ 1);
+      else
+        w4_wait(bar + L::AEMPTY + s, ph ^ 1);
       const uint32_t ab = smem_u32(smem + L::OFF_A) + s * L::A_BYTES;
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {  // 16-byte chunk j = k pairs 4j..4j+3
@@ -727,6 +761,7 @@ __global__ void __launch_bounds__(l12_threads<NH>(), 1)
 // warps 2-9: epilogue, 2 per TMEM lane quarter (column halves)
 // warps 10-17: layer-1 producers (thread = two rows x 8 k pairs)
 constexpr int W4_EPI = 8, W4_PW = 8;
+
 constexpr int W4_THREADS = 32 * (2 + W4_EPI + W4_PW);
 // NS = 2: CTA pair (cta_group::2).  Rank 0 issues M = 256 MMAs over both
 // CTAs' A1 / A3 rings and TMEM; every W box is split along N, each CTA
@@ -879,7 +914,7 @@ __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32
     // R1's last MMAs are issued before R2's (TFULL1), so its drain overlaps them
 #pragma unroll 1
     for (int reg = 0; reg < 2; ++reg) {
-      mbar_wait_sleep(bar + (reg ? L::TFULL : L::TFULL1), i & 1);
+      w4_wait(bar + (reg ? L::TFULL : L::TFULL1), i & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int cc = 0; cc < 2; ++cc) {
@@ -894,7 +929,7 @@ __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32
       warp_arrive_mma<NS>(bar + (reg ? L::R2FREE : L::R1FREE));
     }
     // layer 3 accumulator (R1) -> +b3, act, . w4 over this half's 128 columns
-    mbar_wait_sleep(bar + L::L3FULL, i & 1);
+    w4_wait(bar + L::L3FULL, i & 1);
     tc_fence_after();
     uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll 1
@@ -1032,7 +1067,7 @@ __global__ void __launch_bounds__(W4_THREADS, 1)
     if (lane == 0) {
       int s = 0, ph = 0;
       auto load = [&](const CUtensorMap* map, int k0, int n0) {
-        mbar_wait_sleep(bar + L::BEMPTY + s, ph ^ 1);
+        w4_wait(bar + L::BEMPTY + s, ph ^ 1);
         if (rank == 0) mbar_expect_tx(bar + L::BFULL + s, L::B_BYTES * NS);
         w4_tma<NS>(smem_u32(smem + L::OFF_B + s * L::B_BYTES), map, bar + L::BFULL + s, k0, n0);
         if (++s == L::SB) {
@@ -1305,7 +1340,7 @@ __device__ __forceinline__ void lt_epilogue(uint8_t* smem, uint64_t* bar, uint32
     const int u = blockIdx.x + i * gridDim.x;
     const int64_t m = (int64_t)(u / npass) * GBM + r;
     const int p = u % npass;
-    mbar_wait_sleep(bar + L::TFULL, i & 1);
+    w4_wait(bar + L::TFULL, i & 1);
     tc_fence_after();
     uint4* o = reinterpret_cast<uint4*>(a.out + m * a.H2 + p * 256 + half * 128);
     uint32_t v[2][16];
@@ -1395,7 +1430,7 @@ __global__ void __launch_bounds__(LT_THREADS, 1)
         const int p = (blockIdx.x + i * gridDim.x) % npass;
         for (int kb = 0; kb < KB; ++kb, ++g) {
           const int sb = g % LT_SB;
-          mbar_wait_sleep(bar + L::BEMPTY + sb, ((g / LT_SB) & 1) ^ 1);
+          w4_wait(bar + L::BEMPTY + sb, ((g / LT_SB) & 1) ^ 1);
           mbar_expect_tx(bar + L::BFULL + sb, L::B_BYTES);
           tma_load_2d(smem_u32(smem + L::OFF_B + sb * L::B_BYTES), &tb, bar + L::BFULL + sb, kb * 64, p * 256);
         }
@@ -1900,6 +1935,158 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
       rc = gemm_launch<128, 64, 4, EPI_DOT>(a2, h2, W3, h2, g, out, dst, s);
     else
       rc = fail(SMLRT_E_UNSUPPORTED, "wide path: H3 must be 128 or 256");
+  }
+  cudaFreeAsync(buf, s);
+  return rc;
+}
+
+// ------------------------------------------------ generic tcgen05 layer chain
+// Any dense model at bf16 (models.py:40-64 has no shape restrictions; neither
+// does this path): per block of rows, the in-plan gather writes bf16 rows
+// padded to K0 (16, or a multiple of 64), every hidden layer is one
+// persistent TMA/tcgen05 GEMM with bias + activation + bf16 fused in the
+// epilogue (EPI_BF16, widths padded to multiples of 64 with zero weights, so
+// padded activations are act(0) = 0), and the last layer writes f32 rows
+// (EPI_F32) that the out-plan scatter (or the checked commit's staging)
+// consumes.  The shape-specialised fused kernels (bonds, MiniBUDE) stay the
+// fast path; this is the fallback that keeps every bf16 model runnable.
+namespace {
+
+int chain_k0(int f) { return f <= 16 ? 16 : (f + 63) / 64 * 64; }
+int chain_pad(int n) { return (n + 63) / 64 * 64; }
+
+// gather through any plan into bf16 [rows][k0] (columns >= n_cols are zero)
+__global__ void __launch_bounds__(256) chain_gather_kernel(const __grid_constant__ DevPlan P,
+                                                           const __grid_constant__ Ptrs src, int64_t r0,
+                                                           int64_t rows, int k0, __nv_bfloat16* out) {
+  const int64_t n = rows * k0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = e / k0;
+    const int c = (int)(e - rr * k0);
+    float v = 0.0f;
+    if (c < P.n_cols) {
+      const int a = P.uniform ? P.uarray : __ldg(P.col_arr + c);
+      v = load_as_f32(src.p[a], src.dt[a], element_address(P, (uint32_t)(r0 + rr), c));
+    }
+    out[e] = __float2bfloat16_rn(v);
+  }
+}
+
+template <int EPI>
+int chain_gemm(const void* A, int64_t lda, const void* B, int k_pad, int n_pad, GemmArgs& g, const DevPlan& none,
+               const OutPtrs& dst, cudaStream_t s) {
+  g.K = k_pad;
+  g.N = n_pad;
+  const bool k16 = k_pad == 16;
+  if (n_pad % 256 == 0)
+    return k16 ? gemm_launch<256, 16, 8, EPI>(A, lda, B, k_pad, g, none, dst, s)
+               : gemm_launch<256, 64, 4, EPI>(A, lda, B, k_pad, g, none, dst, s);
+  if (n_pad % 128 == 0)
+    return k16 ? gemm_launch<128, 16, 8, EPI>(A, lda, B, k_pad, g, none, dst, s)
+               : gemm_launch<128, 64, 4, EPI>(A, lda, B, k_pad, g, none, dst, s);
+  return k16 ? gemm_launch<64, 16, 8, EPI>(A, lda, B, k_pad, g, none, dst, s)
+             : gemm_launch<64, 64, 4, EPI>(A, lda, B, k_pad, g, none, dst, s);
+}
+
+}  // namespace
+
+bool chain_ok(const smlrt_model_s& m) {
+  for (const auto& L : m.layers)
+    if (L.kind != SMLRT_DENSE || L.out > 4096) return false;
+  return m.n_layers >= 1;
+}
+
+int chain_pack(smlrt_model_s& m) {
+  if (!chain_ok(m)) return SMLRT_OK;
+  std::vector<uint8_t> blob;
+  const float* p = m.host_params.data();
+  int k = chain_k0(m.in_features);
+  m.chain.clear();
+  for (int l = 0; l < m.n_layers; ++l) {
+    const auto& L = m.layers[l];
+    smlrt_model_s::ChainLayer c{};
+    c.k_pad = k;
+    c.n_pad = chain_pad(L.out);
+    c.n = L.out;
+    c.act = L.act;
+    c.w_off = (blob.size() + 1023) & ~size_t(1023);
+    c.b_off = (c.w_off + (size_t)c.n_pad * c.k_pad * 2 + 255) & ~size_t(255);
+    blob.resize(c.b_off + (size_t)c.n_pad * 4, 0);
+    auto* w = reinterpret_cast<uint16_t*>(blob.data() + c.w_off);
+    for (int n = 0; n < L.out; ++n)
+      for (int kk = 0; kk < L.in; ++kk) w[(size_t)n * c.k_pad + kk] = bf16_bits(p[(size_t)n * L.in + kk]);
+    std::memcpy(blob.data() + c.b_off, p + (size_t)L.out * L.in, (size_t)L.out * 4);
+    p += (size_t)L.out * L.in + L.out;
+    m.chain.push_back(c);
+    k = c.n_pad;
+  }
+  SMLRT_CUDA(cudaMalloc(&m.chain_blob, blob.size()));
+  SMLRT_CUDA(cudaMemcpy(m.chain_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  return SMLRT_OK;
+}
+
+int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
+                        int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
+                        int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
+  if (m.chain_blob == nullptr || m.chain.empty())
+    return fail(SMLRT_E_UNSUPPORTED, "bf16 layer chain: model has non-dense layers or a layer wider than 4096");
+  if (n_in > 8 || n_out > 8) return fail(SMLRT_E_UNSUPPORTED, "bf16 layer chain: more than 8 arrays per plan");
+  Ptrs src{};
+  for (int i = 0; i < n_in; ++i) {
+    src.p[i] = in_ptrs[i];
+    src.dt[i] = in_dt[i];
+  }
+  OutPtrs dst{};
+  int maxw = m.chain[0].k_pad;
+  for (const auto& c : m.chain) maxw = std::max(maxw, c.n_pad);
+  const int G = m.out_features;
+  // rows per block: two bf16 activation buffers + the f32 output stay within 256 MB
+  const int64_t rows = r1 - r0;
+  const int64_t per_row = (int64_t)maxw * 2 * 2 + (int64_t)G * 4;
+  const int64_t ch = std::min<int64_t>(rows, std::max<int64_t>(GBM, ((256ll << 20) / per_row) / GBM * GBM));
+  uint8_t* buf;
+  SMLRT_CUDA(cudaMallocAsync(&buf, (size_t)ch * per_row, s));
+  auto* act0 = reinterpret_cast<__nv_bfloat16*>(buf);
+  auto* act1 = act0 + ch * maxw;
+  auto* y = reinterpret_cast<float*>(act1 + ch * maxw);
+  const uint8_t* wb = reinterpret_cast<const uint8_t*>(m.chain_blob);
+  DevPlan none{};
+  int rc = SMLRT_OK;
+  for (int64_t r = r0; r < r1 && !rc; r += ch) {
+    const int64_t n = std::min(ch, r1 - r);
+    const int k0 = m.chain[0].k_pad;
+    const int blocks = (int)std::min<int64_t>((n * k0 + 255) / 256, 148 * 16);
+    chain_gather_kernel<<<blocks, 256, 0, s>>>(in, src, r, n, k0, act0);
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess) {
+      rc = fail(SMLRT_E_CUDA, "chain gather launch failed");
+      break;
+    }
+    __nv_bfloat16* cur = act0;
+    __nv_bfloat16* nxt = act1;
+    for (int l = 0; l < m.n_layers && !rc; ++l) {
+      const auto& c = m.chain[l];
+      GemmArgs g{};
+      g.M = (int)n;
+      g.act = c.act;
+      g.bias = reinterpret_cast<const float*>(wb + c.b_off);
+      g.status = status;
+      const void* W = wb + c.w_off;
+      if (l + 1 < m.n_layers) {
+        g.out = nxt;
+        g.ldo = c.n_pad;
+        rc = chain_gemm<EPI_BF16>(cur, c.k_pad, W, c.k_pad, c.n_pad, g, none, dst, s);
+        std::swap(cur, nxt);
+      } else {
+        // f32 rows: straight into the checked commit's staging, else a scratch block for the scatter
+        g.out_f32 = staged != nullptr ? staged + (r - r0) * G : y;
+        g.ldo = G;
+        g.n_valid = G;
+        rc = chain_gemm<EPI_F32>(cur, c.k_pad, W, c.k_pad, c.n_pad, g, none, dst, s);
+      }
+    }
+    if (!rc && staged == nullptr)
+      rc = launch_scatter(out, y, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
   }
   cudaFreeAsync(buf, s);
   return rc;

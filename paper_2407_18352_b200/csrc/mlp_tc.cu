@@ -1816,6 +1816,7 @@ __global__ void __launch_bounds__(128, 1) tc_selftest_kernel(const float* A, con
 }  // namespace
 
 int tc_pack_model(smlrt_model_s& m) {
+  if (int rc = chain_pack(m)) return rc;  // the generic fallback of every dense model
   if (wide_shape(m)) return wide_pack(m);
   // [single-CTA blob][pad to 1 KB][rank-0 blob][rank-1 blob]
   std::vector<uint8_t> blob, pair;
@@ -1842,17 +1843,24 @@ int tc_pack_model(smlrt_model_s& m) {
 int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                      int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                      int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status, bool probe_only) {
-  if (m.tc_blob == nullptr && !(probe_only && m.precision == SMLRT_BF16 &&
-                                (shape_is(m, 256, 128) || shape_is(m, 128, 64) || wide_shape(m))))
-    return SMLRT_E_UNSUPPORTED;
-  if (probe_only) return SMLRT_OK;
-  if (wide_shape(m))
-    return launch_region_wide(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
-  if (shape_is(m, 256, 128))
-    return launch<256, 128>(m, in, in_ptrs, in_dt, n_in, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
-  if (shape_is(m, 128, 64))
-    return launch<128, 64>(m, in, in_ptrs, in_dt, n_in, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
-  return SMLRT_E_UNSUPPORTED;
+  // probe_only: is there a shape-specialised fused kernel (the generic chain
+  // is probed with chain_ok)
+  if (probe_only)
+    return m.precision == SMLRT_BF16 && (shape_is(m, 256, 128) || shape_is(m, 128, 64) || wide_shape(m))
+               ? SMLRT_OK
+               : SMLRT_E_UNSUPPORTED;
+  int rc = SMLRT_E_UNSUPPORTED;
+  if (m.tc_blob != nullptr) {
+    if (wide_shape(m))
+      rc = launch_region_wide(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
+    else if (shape_is(m, 256, 128))
+      rc = launch<256, 128>(m, in, in_ptrs, in_dt, n_in, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
+    else if (shape_is(m, 128, 64))
+      rc = launch<128, 64>(m, in, in_ptrs, in_dt, n_in, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
+  }
+  if (rc != SMLRT_E_UNSUPPORTED) return rc;
+  // any other dense model (or plans the specialised kernels do not take)
+  return launch_region_chain(m, in, in_ptrs, in_dt, n_in, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
 }
 
 }  // namespace smlrt
