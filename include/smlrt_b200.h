@@ -158,7 +158,8 @@ int smlrt_model_upload(const smlrt_layer_t* layers, int n_layers,
 int smlrt_model_free(smlrt_model_t model);
 /* which kernel region_infer would run: 0 none, 1 fused exact (templated),
  * 2 unfused exact, 3 fused tcgen05 bf16 (shape-specialised), 4 fused conv
- * front + exact dense, 5 generic tcgen05 bf16 layer chain (any dense model) */
+ * front + exact dense, 5 generic tcgen05 bf16 layer chain (any dense model),
+ * 6 fused exact with runtime dimensions (any small dense MLP) */
 int smlrt_model_path(smlrt_model_t model, int32_t n_in_cols, int32_t* path);
 
 /* gather_batch / concretize_to (bridge.py:388-395, 457-462): rows

@@ -176,9 +176,8 @@ extern "C" int smlrt_model_path(smlrt_model_t m, int32_t n_in_cols, int32_t* pat
       *path = 3;
     else
       *path = chain_ok(*m) ? 5 : 0;
-  } else if (launch_region_exact_fused(*m, dummy, nullptr, nullptr, 0, dummy, nullptr, nullptr, 0, 0,
-                                       0, nullptr, 0, nullptr, true) == SMLRT_OK) {
-    *path = 1;
+  } else if (int k = exact_fused_kind(*m)) {
+    *path = k;
   }
   return SMLRT_OK;
 }

@@ -201,6 +201,8 @@ int launch_region_exact_fused(const smlrt_model_s& m, const DevPlan& in, const v
                               void* const* out_ptrs, const int32_t* out_dt, int n_out,
                               int64_t r0, int64_t r1, float* staged, cudaStream_t s,
                               uint32_t* status, bool probe_only);
+// 1: a templated fused instantiation, 6: the runtime-dims fused kernel, 0: unfused
+int exact_fused_kind(const smlrt_model_s& m);
 // conv2d(+maxpool2d) front + exact dense tail (cnn_exact.cu)
 bool cnn_model(const smlrt_model_s& m);
 int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,

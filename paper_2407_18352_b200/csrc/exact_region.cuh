@@ -517,5 +517,8 @@ int exact_try_c5(const smlrt_model_s&, const DevPlan&, const Ptrs&, const DevPla
                  int64_t, float*, cudaStream_t, uint32_t*, bool, bool*);
 int exact_try_small(const smlrt_model_s&, const DevPlan&, const Ptrs&, const DevPlan&, const Ptrs&, bool, int64_t,
                     int64_t, float*, cudaStream_t, uint32_t*, bool, bool*);
+// any small dense MLP, runtime dimensions (exact_generic.cu)
+int exact_try_generic(const smlrt_model_s&, const DevPlan&, const Ptrs&, const DevPlan&, const Ptrs&, bool, int64_t,
+                      int64_t, float*, cudaStream_t, uint32_t*, bool, bool*);
 
 }  // namespace smlrt

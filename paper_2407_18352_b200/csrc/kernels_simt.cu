@@ -216,10 +216,21 @@ int launch_region_exact_fused(const smlrt_model_s& m, const DevPlan& in, const v
   int rc = SMLRT_OK;
   // Instantiated shapes (one translation unit each): the frozen configs'
   // exact-fp32 models and the reference's analytic models.
-  for (ExactTryFn fn : {exact_try_c1, exact_try_c5, exact_try_small})
+  for (ExactTryFn fn : {exact_try_c1, exact_try_c5, exact_try_small, exact_try_generic})
     if ((rc = fn(m, in, src, out, dst, all_f32, r0, r1, staged, s, status, probe_only, &done)) != SMLRT_OK || done)
       return rc;
   return done ? SMLRT_OK : SMLRT_E_UNSUPPORTED;
+}
+
+int exact_fused_kind(const smlrt_model_s& m) {
+  DevPlan d{};
+  Ptrs p{};
+  bool done = false;
+  for (ExactTryFn fn : {exact_try_c1, exact_try_c5, exact_try_small})
+    if (fn(m, d, p, d, p, true, 0, 0, nullptr, nullptr, nullptr, true, &done) == SMLRT_OK && done) return 1;
+  if (exact_try_generic(m, d, p, d, p, true, 0, 0, nullptr, nullptr, nullptr, true, &done) == SMLRT_OK && done)
+    return 6;
+  return 0;
 }
 
 }  // namespace smlrt

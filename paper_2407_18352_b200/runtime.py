@@ -195,6 +195,7 @@ class Runtime:
         self._staging = _Staging()
         self._side = None  # (host->device, device->host) streams of the chunked host path
         self._collect_side = None  # device->host stream of the collect snapshots
+        self._pinned_bufs: dict = {}  # (region, direction) -> reused pinned host buffer
         self.precision = precision
         self.commit = commit
         self.shard = shard
@@ -355,10 +356,22 @@ class Runtime:
                        torch.cuda.current_stream(self.device).cuda_stream)
         return Tensor(out.reshape(tuple(sweep) + (plan.n_cols,)))
 
-    def _snapshot(self, maps):
+    def _pinned(self, key, shape, dtype) -> torch.Tensor:
+        """Pinned host staging buffer of the collect path, reused across calls
+        (one per region direction; page-locking is the expensive part of a
+        host allocation).  The SRDB append consumes it synchronously, so the
+        next call may overwrite it."""
+        buf = self._pinned_bufs.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape) or buf.dtype != dtype:
+            buf = torch.empty(shape, dtype=dtype, pin_memory=True)
+            self._pinned_bufs[key] = buf
+        return buf
+
+    def _snapshot(self, maps, key=None):
         """Gather on the compute stream, copy to pinned host memory on a side stream."""
         t = self._gather_dense(maps)
-        host = torch.empty(t.data.shape, dtype=t.data.dtype, pin_memory=True)
+        host = self._pinned(key, t.data.shape, t.data.dtype) if key is not None else \
+            torch.empty(t.data.shape, dtype=t.data.dtype, pin_memory=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
         side = self._side_stream()
@@ -378,7 +391,7 @@ class Runtime:
         t0 = time.perf_counter_ns()
         for m, d in zip(desc.in_maps + desc.inout_maps, in_maps):
             self._staging.upload(m.array, d.array)
-        x_host, x_dev = self._snapshot(in_maps)
+        x_host, x_dev = self._snapshot(in_maps, (desc.name, "in"))
         self._sync()
         map_to = _ns_since(t0)
 
@@ -390,7 +403,7 @@ class Runtime:
         t0 = time.perf_counter_ns()
         for m, d in zip(desc.out_maps + desc.inout_maps, out_maps):
             self._staging.upload(m.array, d.array)
-        y_host, y_dev = self._snapshot(out_maps)
+        y_host, y_dev = self._snapshot(out_maps, (desc.name, "out"))
         _native.collect_wait(self._side_stream().cuda_stream)
         map_from = _ns_since(t0)
 

@@ -62,3 +62,33 @@ def test_cnn_model_v2_round_trip(tmp_path):
     for a_, b_ in zip(m.layers, m2.layers):
         if hasattr(a_, "weights"):
             assert a_.weights.tobytes() == b_.weights.tobytes()
+
+
+def test_srdb_read_by_reference_trainer(tmp_path):
+    """The trainer's own reader (trainer/src/smlrt_train/srdb_reader.py:50-82)
+    reads a database this runtime wrote (build container only: the reference
+    checkout is not on the GPU boxes)."""
+    import importlib.util
+    import pytest
+    path = "/root/reference/pkg/trainer/src/smlrt_train/srdb_reader.py"
+    import os
+    if not os.path.exists(path):
+        pytest.skip("reference trainer not present")
+    import sys
+    import types
+    pkg = types.ModuleType("smlrt_train")
+    pkg.__path__ = [os.path.dirname(path)]
+    sys.modules.setdefault("smlrt_train", pkg)
+    spec = importlib.util.spec_from_file_location("smlrt_train.srdb_reader", path)
+    reader = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(reader)
+    rng = np.random.default_rng(0)
+    xs = [rng.random((6, 6, 5), dtype=np.float32) for _ in range(4)]
+    ys = [rng.random((6, 6, 1), dtype=np.float32) for _ in range(4)]
+    with srdb.open_db(tmp_path / "db", "create") as db:
+        for k in range(4):
+            db.append_record("stencil", xs[k], ys[k], 10 + k)
+    ins, outs, times = reader.read_region(tmp_path / "db", "stencil")
+    assert ins.shape == (4, 6, 6, 5) and outs.shape == (4, 6, 6, 1)
+    assert np.array_equal(ins, np.stack(xs)) and np.array_equal(outs, np.stack(ys))
+    assert times.tolist() == [10, 11, 12, 13]
