@@ -274,6 +274,24 @@ def region_infer(pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, f
                                     flags, workspace, stream, status_ptr))
 
 
+def prepare_region(pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, flags, status_ptr, *keep):
+    """A region_infer call with its ctypes arguments built once; returns
+    call(stream) -> 1 if the output was non-finite (SMLRT_SYNC_STATUS) else 0.
+    `keep` holds the objects owning the handles (plans) alive."""
+    fn = lib().smlrt_region_infer
+    args = (pin, _arr(_P, in_ptrs), _arr(_I32, in_dts), pout, _arr(_P, out_ptrs), _arr(_I32, out_dts), model,
+            r0, r1, flags, None)
+
+    def call(stream, _keep=keep):
+        rc = fn(*args, stream, status_ptr)
+        if rc == 0:
+            return 0
+        if rc == 7:  # SMLRT_E_NONFINITE
+            return 1
+        _check(rc)
+    return call
+
+
 def region_workspace(pin, pout, model, rows, flags) -> int:
     n = C.c_size_t()
     _check(lib().smlrt_region_workspace(pin, pout, model, rows, flags, C.byref(n)))

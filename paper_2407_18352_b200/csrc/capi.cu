@@ -288,6 +288,25 @@ extern "C" int smlrt_region_infer(smlrt_plan_t pin, const void* const* in_ptrs, 
   if (dev != m->device) return fail(SMLRT_E_INVALID, "region_infer: model lives on another device");
   cudaStream_t s = (cudaStream_t)stream;
   if (flags & SMLRT_SYNC_STATUS) {
+    if (!(flags & SMLRT_COMMIT_CHECKED)) {
+      // zero-copy status: a mapped pinned word the kernels store into, reset
+      // by the host -- launch + sync only, no memset or read-back copy
+      static thread_local volatile uint32_t* h_flag = nullptr;  // one per host thread
+      if (!h_flag) {
+        void* p = nullptr;
+        SMLRT_CUDA(cudaHostAlloc(&p, sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+        h_flag = static_cast<volatile uint32_t*>(p);
+      }
+      uint32_t* d_flag = nullptr;
+      SMLRT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_flag), const_cast<uint32_t*>(h_flag), 0));
+      *h_flag = 0u;
+      const int rc = region_launch(pin, in_ptrs, in_dt, pout, out_ptrs, out_dt, m, r0, r1, flags, workspace, s, d_flag);
+      if (rc) return rc;
+      SMLRT_CUDA(cudaStreamSynchronize(s));
+      if (*h_flag & SMLRT_STATUS_NONFINITE) return fail(SMLRT_E_NONFINITE, "forward pass produced NaN/inf");
+      return SMLRT_OK;
+    }
+    // checked commit: the gated scatter reads the status word, keep it in HBM
     SMLRT_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t), s));
     const int rc = region_launch(pin, in_ptrs, in_dt, pout, out_ptrs, out_dt, m, r0, r1, flags, workspace, s, status);
     if (rc) return rc;

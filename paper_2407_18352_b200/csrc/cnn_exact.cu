@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
     }
   }
   if (status != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
-    atomicOr(status, SMLRT_STATUS_NONFINITE);
+    flag_nonfinite(status);
 }
 
 int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const void* src, int src_dt,

@@ -146,6 +146,13 @@ struct smlrt_plan_s {
 
 namespace smlrt {
 
+// Raise the non-finite bit of a status word: a plain store (every writer
+// stores the same bit, no read-modify-write needed), so the word may also live
+// in mapped host memory (the synchronous call's zero-copy status flag).
+__device__ __forceinline__ void flag_nonfinite(uint32_t* status) {
+  *reinterpret_cast<volatile uint32_t*>(status) = SMLRT_STATUS_NONFINITE;
+}
+
 // kernels launched by this library since load (smlrt_launch_count): the bench
 // reports how many of its own launches a timed region made
 extern std::atomic<unsigned long long> g_launches;

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(T) region_generic_exact_kernel(const __grid_co
       }
     }
   }
-  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(status, SMLRT_STATUS_NONFINITE);
+  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) flag_nonfinite(status);
 }
 
 template <int T>

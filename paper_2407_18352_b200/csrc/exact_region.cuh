@@ -449,7 +449,7 @@ __global__ void SMLRT_EXACT_LB region_exact_kernel(
       }
     }
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(status, SMLRT_STATUS_NONFINITE);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_nonfinite(status);
 }
 
 template <int... D>

@@ -164,7 +164,7 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
             }
           }
         }
-        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(g.status, SMLRT_STATUS_NONFINITE);
+        if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(g.status);
       } else if constexpr (EPI == EPI_BF16) {
         uint32_t p[16];
 #pragma unroll
@@ -260,7 +260,7 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
             reinterpret_cast<double*>(dst.p[arr])[addr] = (double)y;
         }
       }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(g.status, SMLRT_STATUS_NONFINITE);
+      if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(g.status);
     }
   }
 }
@@ -989,7 +989,7 @@ __device__ __forceinline__ void w4_epilogue(uint8_t* smem, uint64_t* bar, uint32
             reinterpret_cast<double*>(dst.p[arr])[addr] = (double)y;
         }
       }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+      if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(a.status);
     }
   }
 }

@@ -80,6 +80,31 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
   }
 }
 
+// Uniform plans: one thread per row -- one row offset per row instead of one
+// unravel per element, column offsets from the parameter bank; the staged
+// row is read contiguously and every column's stores are coalesced across
+// the warp (the checked commit's scatter of C5's 4-plane output).
+template <typename InT>
+__global__ void __launch_bounds__(kThreads) scatter_rows_kernel(const __grid_constant__ DevPlan P,
+                                                                const InT* __restrict__ in,
+                                                                const __grid_constant__ Ptrs dst, int64_t r0,
+                                                                int64_t rows, const uint32_t* gate) {
+  if (gate != nullptr && *gate != 0u) return;
+  const int G = P.n_cols;
+  void* base = const_cast<void*>(dst.p[P.uarray]);
+  const int dt = dst.dt[P.uarray];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ro = row_offset_uniform(P, (uint32_t)(r0 + i));
+    const InT* v = in + i * G;
+    for (int c = 0; c < G; ++c) {
+      if constexpr (sizeof(InT) == 4)
+        store_f32(base, dt, P.col_inl[c] + ro, v[c]);
+      else
+        store_f64(base, dt, P.col_inl[c] + ro, v[c]);
+    }
+  }
+}
+
 // ------------------------------------------------------ dense layer (exact) --
 // Thread per (row, block of TJ outputs); weights are warp-uniform loads.
 template <int TJ>
@@ -113,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) dense_exact_kernel(const float* __re
     }
   }
   if (status != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
-    atomicOr(status, SMLRT_STATUS_NONFINITE);
+    flag_nonfinite(status);
 }
 
 template <typename S, typename D>
@@ -166,7 +191,13 @@ int launch_scatter(const DevPlan& p, const void* in, int in_dtype, void* const* 
   int64_t n = (r1 - r0) * (int64_t)p.n_cols;
   if (n <= 0) return SMLRT_OK;
   Ptrs dst = pack((const void* const*)ptrs, dtypes, n_arrays);
-  if (in_dtype == SMLRT_F32)
+  if (p.uniform && p.n_cols <= SMLRT_INLINE_COLS) {
+    const int64_t rows = r1 - r0;
+    if (in_dtype == SMLRT_F32)
+      scatter_rows_kernel<float><<<grid_for(rows), kThreads, 0, s>>>(p, (const float*)in, dst, r0, rows, gate);
+    else
+      scatter_rows_kernel<double><<<grid_for(rows), kThreads, 0, s>>>(p, (const double*)in, dst, r0, rows, gate);
+  } else if (in_dtype == SMLRT_F32)
     scatter_kernel<float><<<grid_for(n), kThreads, 0, s>>>(p, (const float*)in, dst, r0, n, gate);
   else
     scatter_kernel<double><<<grid_for(n), kThreads, 0, s>>>(p, (const double*)in, dst, r0, n, gate);

@@ -227,7 +227,7 @@ struct Sched {
 template <bool PAIR>
 __device__ __forceinline__ void arrive_mma(uint64_t* bar) {
   if constexpr (PAIR)
-    mbar_arrive_cluster(mapa(bar, 0));
+    mbar_arrive_remote(mapa(bar, 0));
   else
     mbar_arrive(bar);
 }
@@ -510,7 +510,7 @@ __device__ __forceinline__ void epilogue2(uint8_t* smem, uint64_t* bar, uint32_t
           reinterpret_cast<double*>(base)[addr] = (double)y;
       }
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(a.status);
     if (q == 0 && lane == 0) TR(7, it);
   }
 }
@@ -765,8 +765,8 @@ __global__ void __launch_bounds__(ss_threads<PAIR>(), 1)
     const uint64_t w20d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
     auto issue_l2 = [&](int j) {
       const int b = j & 1;
-      mbar_wait_cluster(bar + L::B_A2FULL + b, (j >> 1) & 1);
-      mbar_wait_cluster(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
+      mbar_wait(bar + L::B_A2FULL + b, (j >> 1) & 1);
+      mbar_wait(bar + L::B_L2EMPTY + b, ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tbase + L::T_L2 + b * H2;
       const uint64_t ab = a20d + ((b * L::A2_BUF) >> 4);
@@ -782,8 +782,8 @@ __global__ void __launch_bounds__(ss_threads<PAIR>(), 1)
     };
     for (int it = 0; it < n_my; ++it) {
       const int s = it % XSTAGES;
-      mbar_wait_cluster(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
-      mbar_wait_cluster(bar + L::B_L1EMPTY, (it & 1) ^ 1);
+      mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
+      mbar_wait(bar + L::B_L1EMPTY, (it & 1) ^ 1);
       tc_fence_after();
       mma2_ss_elect(tbase + L::T_L1, onesd, w1bd, idesc1, 0);  // D = b1
       mma2_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d, idesc1, 1);
@@ -1285,7 +1285,7 @@ __device__ __forceinline__ void epilogue2_ts2(uint8_t* smem, uint64_t* bar, uint
           reinterpret_cast<double*>(base)[addr] = (double)y;
       }
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(a.status);
   }
 }
 

@@ -196,6 +196,7 @@ class Runtime:
         self._side = None  # (host->device, device->host) streams of the chunked host path
         self._collect_side = None  # device->host stream of the collect snapshots
         self._pinned_bufs: dict = {}  # (region, direction) -> reused pinned host buffer
+        self._fast: dict = {}  # region -> (key, prepared native call) of device-resident regions
         self.precision = precision
         self.commit = commit
         self.shard = shard
@@ -262,6 +263,7 @@ class Runtime:
 
     def unload_models(self):
         """Drop cached models; the next inference reloads from disk."""
+        self._fast.clear()
         self._models.clear()
         self._realpaths.clear()
 
@@ -450,10 +452,22 @@ class Runtime:
         self._plans[desc.name] = (key, pin, pout, batch_rows)
         return pin, pout, batch_rows
 
+    def _fast_key(self, desc, model):
+        """What a prepared call depends on: the bound arrays' storage and
+        geometry, the functors/targets, the model object and the runtime's
+        settings.  Equal keys -> the cached native arguments are still valid."""
+        maps = desc.in_maps + desc.out_maps + desc.inout_maps
+        return (id(model), self.precision, self.commit, self.shard,
+                tuple((id(m.array.data), m.array.data.data_ptr(), m.array.data.dtype, m.array.shape,
+                       m.array.strides, id(m.functor), id(m.target)) for m in maps))
+
     def _run_surrogate(self, desc, st) -> RegionOutcome:
         model = self._model_for(desc)
         if self.device is None:
             raise RuntimeError("no CUDA device: the B200 runtime has no CPU data path")
+        fast = self._fast.get(desc.name)
+        if fast is not None and not self.time_kernels and fast[0] == self._fast_key(desc, model):
+            return self._run_prepared(fast[1], st)
         host_in = desc.in_maps + desc.inout_maps
         host_out = desc.out_maps + desc.inout_maps
         t0 = time.perf_counter_ns()
@@ -503,6 +517,12 @@ class Runtime:
         sync_native = not self.time_kernels and all(m.array.is_device for m in host_out)
         if sync_native:
             flags |= _native.SYNC_STATUS
+            # device-resident region: later calls with the same arrays, model
+            # and settings skip straight to the native call with these arguments
+            if all(m.array.is_device for m in host_in):
+                self._fast[desc.name] = (self._fast_key(desc, model), _native.prepare_region(
+                    pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1, flags, status.data_ptr(),
+                    pin, pout, model))
         else:
             status.zero_()
         if self.time_kernels:
@@ -534,6 +554,18 @@ class Runtime:
         return RegionOutcome(path_taken=SURROGATE, elapsed_region_ns=infer_ns,
                              elapsed_map_to_ns=map_to, elapsed_map_from_ns=map_from,
                              elapsed_infer_ns=infer_ns)
+
+    def _run_prepared(self, call, st) -> RegionOutcome:
+        """The steady-state surrogate call: one native call (status reset,
+        fused launch, status read-back, stream sync) with cached arguments."""
+        t0 = time.perf_counter_ns()
+        bad = call(torch._C._cuda_getCurrentRawStream(self.device.index))
+        infer_ns = _ns_since(t0)
+        if bad:
+            raise NonFiniteOutputError("forward pass produced NaN/inf")
+        st.surrogate_calls += 1
+        st.infer_ns += infer_ns
+        return RegionOutcome(path_taken=SURROGATE, elapsed_region_ns=infer_ns, elapsed_infer_ns=infer_ns)
 
     # host-resident (pinned) input and output over uniform 1-D plans (AoS rows
     # or SoA columns): the row range is cut into chunks whose host->device

@@ -332,3 +332,100 @@ def test_in_and_out_maps_on_one_array_use_pre_call_state(cuda, jdir, host):
     got = (t.data.numpy() if host else t.to_numpy()).reshape(n, n)
     assert np.array_equal(got[1:-1, 1:-1], jacobi_ref(f0))
     assert np.array_equal(got[0], f0[0]) and np.array_equal(got[:, -1], f0[:, -1])
+
+
+def test_aos_in_place_1d_not_chunked_and_exact(cuda, tmp_path):
+    """One pinned AoS buffer read (fields 0-4) and written (field 5) by the
+    same region: disjoint fields of a shared buffer are not 'shared storage'
+    (element-level check), every other element is left untouched, the output
+    matches the device-resident run."""
+    from paper_2407_18352_b200 import workloads
+    n = 50_000
+    rng = np.random.default_rng(1)
+    recs = rng.uniform(0.1, 1.0, (n, 6)).astype(np.float32)
+    wl = workloads.make("options", 16)
+    sm.save_model(wl.model, tmp_path / "m")
+    env = {"N": n}
+    fi = sm.parse_directive("functor(fi: [k, 0:5] = ([k, 0:5]))")
+    fo = sm.parse_directive("functor(fo: [k, 0:1] = ([k, 5]))")
+    ti = sm.parse_directive("map(to: fi(r[0:N]))", env).targets[0]
+    tf = sm.parse_directive("map(from: fo(r[0:N]))", env).targets[0]
+    outs = []
+    for host in (False, True):
+        if host:
+            buf = sm.ArrayBuffer(torch.from_numpy(recs.reshape(-1).copy()).pin_memory(), (n, 6), (6, 1))
+        else:
+            buf = sm.ArrayBuffer.from_numpy(recs)
+        desc = sm.RegionDescriptor(name="aos", accurate_fn=lambda: None,
+                                   ml=sm.parse_ml_clause(f'ml(infer) in(r) out(r) model("{tmp_path / "m"}")'),
+                                   in_maps=[sm.BoundMap(fi, ti, buf)], out_maps=[sm.BoundMap(fo, tf, buf)], env=env)
+        with sm.Runtime() as rt:
+            rt.STREAM_MIN_BYTES = 0
+            rt.invoke_region(rt.register_region(desc))
+            pin, pout = rt._plans["aos"][1], rt._plans["aos"][2]
+            from paper_2407_18352_b200.runtime import _shares_storage
+            assert not _shares_storage(pin, pout)
+        outs.append(buf.data.numpy().reshape(n, 6).copy() if host else buf.to_numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0][:, :5], recs[:, :5])
+    from oracle import oracle
+    want, _ = oracle.infer(wl.layers, recs[:, :5])
+    assert np.array_equal(outs[0][:, 5], want[:, 0])
+
+
+@pytest.mark.parametrize("mode", ["shard", "checked_nan"])
+def test_host_output_untouched_where_not_written(cuda, tmp_path, mode):
+    """Host (pinned, non-chunked: below the size floor) output buffers: rows
+    outside this rank's shard, or everything on a checked commit that hits a
+    non-finite output, keep their host values (the device mirror is
+    downloaded whole, so it must be uploaded first)."""
+    from paper_2407_18352_b200 import workloads
+    n = 10_000
+    wl = workloads.make("options", n)
+    wl.to_device(pinned_host=True)
+    _, _, ti, to = wl.functors()
+    wl.buffers[to.array].data[:] = 123.0
+    if mode == "checked_nan":
+        wl.buffers[ti.array].data[7] = float("nan")
+    sm.save_model(wl.model, tmp_path / "m")
+    rt = sm.Runtime(shard=(1, 2)) if mode == "shard" else sm.Runtime(commit="checked")
+    with rt:
+        h = rt.register_region(wl.descriptor(str(tmp_path / "m")))
+        if mode == "shard":
+            rt.invoke_region(h)
+        else:
+            with pytest.raises(NonFiniteOutputError):
+                rt.invoke_region(h)
+    out = wl.buffers[to.array].data.numpy()
+    if mode == "shard":
+        half = (n + 1) // 2
+        assert (out[:half] == 123.0).all() and not (out[half:] == 123.0).any()
+    else:
+        assert (out == 123.0).all()
+
+
+def test_prepared_fast_path(cuda, tmp_path, jdir):
+    """Steady-state calls reuse the prepared native call; a new array bound to
+    the descriptor, a NaN input and unload_models all behave as on the first
+    call."""
+    desc, t, tnew, _ = make_region("infer", model=jdir)
+    with sm.Runtime() as rt:
+        h = rt.register_region(desc)
+        rt.invoke_region(h)
+        assert "stencil" in rt._fast
+        for _ in range(3):
+            rt.invoke_region(h)
+        assert np.array_equal(tnew.to_numpy()[1:-1, 1:-1], jacobi_ref(t.to_numpy()))
+        # rebind the input to a different array
+        t2 = sm.ArrayBuffer.from_numpy(field(5))
+        desc.in_maps[0] = sm.BoundMap(IF, TO, t2)
+        rt.invoke_region(h)
+        assert np.array_equal(tnew.to_numpy()[1:-1, 1:-1], jacobi_ref(t2.to_numpy()))
+        t2.data[7] = float("nan")
+        with pytest.raises(NonFiniteOutputError):
+            rt.invoke_region(h)
+        t2.data[7] = 0.5
+        rt.unload_models()
+        rt.invoke_region(h)
+        assert rt.stats(h).model_loads == 2
+        assert np.array_equal(tnew.to_numpy()[1:-1, 1:-1], jacobi_ref(t2.to_numpy()))
