@@ -16,12 +16,20 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include <cstring>
 
+#include <cuda.h>
+
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace smlrt {
+
+int make_map_f32_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                    uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, int promote);
+
 namespace {
 
 __device__ __forceinline__ float act_exact(float y, int act) {
@@ -288,6 +296,83 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
   }
 }
 
+// The same C4 front with the 128 x 128 window brought in by ONE TMA load per
+// frame (3-D tensor map over [frames][rows][pitch], box 1 x 128 x 128 at the
+// window origin, no L2 sector promotion) instead of 16 LDG.128 per thread:
+// the LDG path fetched whole 128-B lines around each 512-B window row (640 B
+// of a 640-B frame row: 1.25x the window bytes from DRAM).  Each thread then
+// reads its 8 x 8 patch from shared memory, the two 16-B halves of a patch
+// row in lane-dependent order so the 8 lanes of a quarter-warp hit distinct
+// bank groups.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(256) conv_pool_tma_kernel(const __grid_constant__ CUtensorMap tm,
+                                                            const __grid_constant__ FrontArgs a, int x0, int y0,
+                                                            int64_t z0, const __grid_constant__ ConvW8 cw) {
+  extern __shared__ __align__(128) float win[];  // [128][128]
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int py = 2 * warp + (lane >> 4), px = lane & 15;
+  const int64_t row = a.r0 + blockIdx.x;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::mbar_fence_init();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ptx::smem_u32(&bar)), "r"(128 * 128 * 4)
+                 : "memory");
+    tma_load_3d(ptx::smem_u32(win), &tm, &bar, x0, y0, (int)(z0 + row));
+  }
+  __syncthreads();
+  ptx::mbar_wait(&bar, 0);
+  const float* prow = win + (py * 8) * 128 + px * 8;
+  const int h = (px >> 2) & 1;  // which 16-B half first: distinct banks per quarter-warp
+  uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int dy = 0; dy < 8; ++dy) {
+    const float4 f0 = *reinterpret_cast<const float4*>(prow + dy * 128 + 4 * h);
+    const float4 f1 = *reinterpret_cast<const float4*>(prow + dy * 128 + 4 * (h ^ 1));
+    const float4 lo = h ? f1 : f0, hi = h ? f0 : f1;
+    const float v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int dx = 0; dx < 8; ++dx) {
+      const uint64_t vv = cpk2(v[dx], v[dx]);
+      const float* wf = cw.w + (dy * 8 + dx) * 8;
+#pragma unroll
+      for (int op = 0; op < 4; ++op)
+        acc[op] = cadd2(acc[op], cmul2(vv, *reinterpret_cast<const uint64_t*>(wf + 2 * op)), cw.one2);
+    }
+  }
+  float y[8];
+#pragma unroll
+  for (int op = 0; op < 4; ++op) {
+    cupk2(cadd2(acc[op], *reinterpret_cast<const uint64_t*>(cw.b + 2 * op), cw.one2), y[2 * op], y[2 * op + 1]);
+    y[2 * op] = act_exact(y[2 * op], a.act);
+    y[2 * op + 1] = act_exact(y[2 * op + 1], a.act);
+  }
+  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  if (a.pool == 2) {
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      float m = max_nan(y[o], __shfl_xor_sync(0xffffffffu, y[o], 1));
+      m = max_nan(m, __shfl_xor_sync(0xffffffffu, m, 16));
+      y[o] = m;
+    }
+    if (lane < 16 && (lane & 1) == 0) {
+#pragma unroll
+      for (int o = 0; o < 8; ++o) orow[o * 64 + warp * 8 + (lane >> 1)] = y[o];
+    }
+  } else {
+#pragma unroll
+    for (int o = 0; o < 8; ++o) orow[o * 256 + py * 16 + px] = y[o];
+  }
+}
+
 // ------------------------------------------------------------ tiled dense --
 // Exact dense layer on output pairs: thread = 4 rows x 4 columns (2 column
 // pairs), each multiply-accumulate a packed mul.rn.f32x2 + fma.rn.f32x2(p, 1,
@@ -422,7 +507,8 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
 }
 
 int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const void* src, int src_dt,
-                 int64_t r0, int64_t r1, float* out, int* out_w, int* next_layer, cudaStream_t s) {
+                 int64_t r0, int64_t r1, float* out, int* out_w, int* next_layer, cudaStream_t s,
+                 int64_t src_array_elems = 0) {
   const DevLayer& c = m.layers[0];
   FrontArgs a{};
   a.x = x;
@@ -471,8 +557,41 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
     for (int o = 0; o < 8; ++o) cw.b[o] = hw[64 * 8 + o];
     const float one[2] = {1.0f, 1.0f};
     std::memcpy(&cw.one2, one, sizeof(one));
-    conv_pool_k8oc8_kernel<<<(unsigned)(r1 - r0), 256, 0, s>>>(a, P ? *P : dummy, cw);
-    count_launch();
+    // SMLRT_PF_TMA=1 (no L2 promotion) / 2 (128-B promotion): the window by
+    // one TMA load per frame.  Measured on C4: DRAM reads 1.342 GB in all
+    // three modes (L2 sees 640 B per 512-B window row either way: the rows
+    // start 64 B into a 128-B line), kernel time equal (0.324 ms region) --
+    // the over-fetch is the window's line alignment, not the load path.
+    // Default: the LDG kernel (no shared memory, higher occupancy).
+    static const int tma_mode = [] {
+      const char* e = std::getenv("SMLRT_PF_TMA");
+      return e ? std::atoi(e) : 0;
+    }();
+    bool launched = false;
+    if (tma_mode && P != nullptr && a.x == nullptr && P->n_sweep == 1 && P->win_pitch > 0 &&
+        P->ustride[0] % P->win_pitch == 0 && src_array_elems > 0) {
+      const int64_t pitch = P->win_pitch, fs = P->ustride[0];
+      const int64_t z0 = P->col_off0 / fs, rem = P->col_off0 % fs;
+      const int x0 = (int)(rem % pitch), y0 = (int)(rem / pitch);
+      const int64_t nz = src_array_elems / fs;
+      CUtensorMap tm;
+      if (x0 + 128 <= pitch && y0 + 128 <= fs / pitch && nz >= z0 + r1 &&
+          make_map_f32_3d(&tm, src, (uint64_t)pitch, (uint64_t)(fs / pitch), (uint64_t)nz, (uint64_t)pitch * 4,
+                          (uint64_t)fs * 4, 128, 128, 1, tma_mode == 2 ? 128 : 0) == SMLRT_OK) {
+        static int cfg = 0;
+        if (!cfg) {
+          SMLRT_CUDA(cudaFuncSetAttribute(conv_pool_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+          cfg = 1;
+        }
+        conv_pool_tma_kernel<<<(unsigned)(r1 - r0), 256, 65536, s>>>(tm, a, x0, y0, z0, cw);
+        count_launch();
+        launched = true;
+      }
+    }
+    if (!launched) {
+      conv_pool_k8oc8_kernel<<<(unsigned)(r1 - r0), 256, 0, s>>>(a, P ? *P : dummy, cw);
+      count_launch();
+    }
   } else if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned) {
     conv_front_fixed_kernel<8, 8><<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
     count_launch();
@@ -555,25 +674,33 @@ int infer_cnn_dense(const smlrt_model_s& m, const float* x, int64_t rows, float*
 }
 
 namespace {
-// side stream per device for the conv front of the overlapped CNN region
-cudaStream_t front_stream(int dev) {
+// per device: a lowest-priority stream for the conv fronts and a
+// highest-priority stream for the dense tails of the overlapped CNN region
+// (the block scheduler hands freed SM slots to the dense tail's CTAs first)
+cudaStream_t cnn_stream(int dev, int which) {
   static std::mutex mu;
-  static cudaStream_t st[64] = {};
+  static cudaStream_t st[64][2] = {};
   std::lock_guard<std::mutex> g(mu);
   if (dev < 0 || dev >= 64) return nullptr;
-  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) st[dev] = nullptr;
-  return st[dev];
+  if (!st[dev][which]) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (cudaStreamCreateWithPriority(&st[dev][which], cudaStreamNonBlocking, which ? greatest : least) != cudaSuccess)
+      st[dev][which] = nullptr;
+  }
+  return st[dev][which];
 }
 }  // namespace
 
 // Rows are processed in chunks of <= 16384 on the caller's stream.
-// Experiment (SMLRT_CNN_CHUNKS=k > 1, off by default): k chunks alternating
-// between two feature buffers, the conv front (HBM-bound) of chunk c+1 on a
-// side stream while the dense tail (FP32-bound) of chunk c runs on the
-// caller's stream, ordered by events (front c waits for the tail of c-2,
-// which read the same buffer).  Measured on C4 (16,384 windows): 1 / 2 / 3 / 4
-// chunks -> 0.330 / 0.397 / 0.416 / 0.443 ms -- the conv grid fills every SM,
-// so the kernels barely co-run and the smaller dense grids lose more.
+// SMLRT_CNN_CHUNKS=k > 1 (experiment, off): k chunks, each with its own
+// feature buffer; the conv fronts (HBM-bound) run in order on a low-priority
+// stream, the dense tail + scatter of chunk c (FP32-bound) on a high-priority
+// stream as soon as front c is done, so the tail of c may co-run with the
+// front of c+1.  Measured on C4 (16,384 windows, region ms): 1 / 2 / 4 / 8 /
+// 16 chunks -> 0.324 / 0.354 / 0.402 / 0.640 / 1.162: a chunk's dense tail
+// is a 64-rows-per-CTA grid too small to spread over the SMs the fronts
+// leave, so it serialises.
 int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                       int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                       int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
@@ -585,55 +712,64 @@ int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* con
   }();
   const int64_t rows = r1 - r0;
   if (rows <= 0) return SMLRT_OK;
-  // >= 4096 rows per chunk keeps the dense tail's grid >= 64 CTAs
-  const int64_t ch = n_chunks > 1
-                         ? std::min<int64_t>(16384, std::max<int64_t>(4096, (rows + n_chunks - 1) / n_chunks))
-                         : std::min<int64_t>(16384, rows);
-  const int nbuf = n_chunks > 1 && rows > ch ? 2 : 1;
+  const int64_t ch = n_chunks > 1 ? std::max<int64_t>(1024, (rows + n_chunks - 1) / n_chunks)
+                                  : std::min<int64_t>(16384, rows);
+  const bool overlap = n_chunks > 1 && rows > ch;
+  const int64_t nb = overlap ? (rows + ch - 1) / ch : 1;  // feature buffers (one per chunk when overlapped)
   size_t per = 1;  // widest activation after the conv front
   for (int l = 1; l < m.n_layers; ++l) per = std::max(per, (size_t)m.layers[l].out);
   const size_t slot = per * 3 + m.out_features;  // f, t0, t1, y per row
   float* buf;
-  SMLRT_CUDA(cudaMallocAsync(&buf, slot * ch * 4 * nbuf, s));
+  SMLRT_CUDA(cudaMallocAsync(&buf, slot * ch * 4 * nb, s));
   int dev = 0;
   SMLRT_CUDA(cudaGetDevice(&dev));
-  cudaStream_t s2 = nbuf > 1 ? front_stream(dev) : nullptr;
-  cudaEvent_t ev[5] = {};  // [0] start, [1..2] front done per buffer, [3..4] tail done per buffer
-  if (s2) {
-    for (auto& e : ev) SMLRT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    SMLRT_CUDA(cudaEventRecord(ev[0], s));
-    SMLRT_CUDA(cudaStreamWaitEvent(s2, ev[0], 0));
+  cudaStream_t sa = overlap ? cnn_stream(dev, 0) : s;
+  cudaStream_t sb = overlap ? cnn_stream(dev, 1) : s;
+  if (!sa || !sb) sa = sb = s;
+  std::vector<cudaEvent_t> ev;
+  auto event = [&]() {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ev.push_back(e);
+    return e;
+  };
+  if (sa != s) {
+    cudaEvent_t e0 = event();
+    SMLRT_CUDA(cudaEventRecord(e0, s));
+    SMLRT_CUDA(cudaStreamWaitEvent(sa, e0, 0));
+    SMLRT_CUDA(cudaStreamWaitEvent(sb, e0, 0));
   }
   int rc = SMLRT_OK;
   int c = 0;
   for (int64_t r = r0; r < r1 && !rc; r += ch, ++c) {
     const int64_t n = std::min(ch, r1 - r);
-    const int b = c % nbuf;
-    float* f = buf + slot * ch * b;
+    float* f = buf + slot * ch * (c % nb);
     float* t0 = f + per * ch;
     float* t1 = t0 + per * ch;
     float* yo = t1 + per * ch;
-    cudaStream_t fs = s2 ? s2 : s;
-    if (s2 && c >= 2) SMLRT_CUDA(cudaStreamWaitEvent(s2, ev[3 + b], 0));
     int ow, nl;
-    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, fs);
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, sa,
+                      in.uarray_numel);
     if (rc) break;
-    if (s2) {
-      SMLRT_CUDA(cudaEventRecord(ev[1 + b], s2));
-      SMLRT_CUDA(cudaStreamWaitEvent(s, ev[1 + b], 0));
+    if (sa != sb) {
+      cudaEvent_t e = event();
+      SMLRT_CUDA(cudaEventRecord(e, sa));
+      SMLRT_CUDA(cudaStreamWaitEvent(sb, e, 0));
     }
     float* ydst = staged ? staged + (r - r0) * m.out_features : yo;
-    rc = dense_tail(m, nl, f, n, ydst, t0, t1, s, status);
+    rc = dense_tail(m, nl, f, n, ydst, t0, t1, sb, status);
     if (rc) break;
-    if (!staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
-    if (s2) SMLRT_CUDA(cudaEventRecord(ev[3 + b], s));
+    if (!staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, sb, nullptr);
   }
-  if (s2) {
-    // the caller's stream owns the buffer again only after the side stream's last work
-    cudaEventRecord(ev[0], s2);
-    cudaStreamWaitEvent(s, ev[0], 0);
-    for (auto& e : ev) cudaEventDestroy(e);
+  if (sa != s) {
+    // the caller's stream continues after both side streams' work
+    cudaEvent_t ea = event(), eb = event();
+    cudaEventRecord(ea, sa);
+    cudaEventRecord(eb, sb);
+    cudaStreamWaitEvent(s, ea, 0);
+    cudaStreamWaitEvent(s, eb, 0);
   }
+  for (auto& e : ev) cudaEventDestroy(e);
   cudaFreeAsync(buf, s);
   (void)n_in;
   return rc;

@@ -71,6 +71,7 @@ struct DevPlan {
   int64_t col_off0;         // col_off[0] (host copy, for launch-time decisions)
   int32_t win_w;            // >0: columns form a 2-D window of rows of win_w
   int64_t win_pitch;        //     elements at this pitch (uniform plans)
+  int64_t uarray_numel;     // uniform: elements of the single array (plan-time extent)
   int64_t col_inl[SMLRT_INLINE_COLS];  // col_off copy in the parameter bank (n_cols <= SMLRT_INLINE_COLS)
 };
 
@@ -126,6 +127,7 @@ struct smlrt_plan_s {
   int n_arrays = 0;
   int n_cols = 0;
   std::vector<smlrt_view_t> views;
+  std::vector<int64_t> array_numel;  // storage extents the plan was validated against
   std::vector<int64_t> col_off;
   std::vector<int32_t> col_arr;
   std::vector<int64_t> col_str;  // n_cols * n_sweep

@@ -2092,4 +2092,25 @@ int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* c
   return rc;
 }
 
+// f32 3-D tensor map (the C4 frame windows): dims {d0 (contiguous), d1, d2},
+// byte strides of dims 1 and 2, box {b0, b1, b2}; no swizzle, no L2 promotion
+// (a window's partial 128-B lines are fetched as sectors, not whole lines)
+int make_map_f32_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                    uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, int promote) {
+  EncodeFn enc = encoder();
+  if (!enc) return fail(SMLRT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapL2promotion pr = promote == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                  : promote == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                  : promote == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SMLRT_E_CUDA, "cuTensorMapEncodeTiled (3-D f32) failed: " + std::to_string((int)r));
+  return SMLRT_OK;
+}
+
 }  // namespace smlrt

@@ -98,6 +98,7 @@ int smlrt_plan_s::tables(DevPlan* p) {
   p->col_off0 = col_off.empty() ? 0 : col_off[0];
   p->win_w = win_w;
   p->win_pitch = win_pitch;
+  p->uarray_numel = uniform && uarray < (int)array_numel.size() ? array_numel[uarray] : 0;
   for (int c = 0; c < n_cols && c < SMLRT_INLINE_COLS; ++c) p->col_inl[c] = col_off[c];
   p->col_off = it->second.col_off;
   p->col_arr = it->second.col_arr;
@@ -133,6 +134,7 @@ extern "C" int smlrt_plan_create(const smlrt_view_t* views, int n_views, int n_s
     return fail(SMLRT_E_UNSUPPORTED, "plan_create: more than 2^32 sweep rows per plan; shard it");
   }
   p->views.assign(views, views + n_views);
+  p->array_numel.assign(array_numel, array_numel + n_arrays);
 
   // ---- bounds (flat) and column table ----
   for (int v = 0; v < n_views; ++v) {
