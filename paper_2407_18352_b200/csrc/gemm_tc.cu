@@ -1192,311 +1192,6 @@ __global__ void __launch_bounds__(W4_THREADS, 1)
   }
 }
 
-// ---------------------------------- fused layers 1 + 2, layer 1 on tcgen05
-// Same contract as l12_fused_kernel, but layer 1 runs on the tensor core too:
-// per 64-wide K chunk of layer 2, one M=128 N=64 K=16 MMA computes the chunk
-// of X W1^T into a (double-buffered) 64-column TMEM region; four "A-producer"
-// warps drain it (+b1, act, bf16) into the SW128 A ring.  That takes the
-// layer-1 FFMAs and their broadcast weight loads off the CUDA cores and the
-// shared-memory read port (which limited l12_fused_kernel to ~50 % tensor
-// activity).  A work unit is (128-row tile, 256-column pass of layer 2); the
-// layer-2 accumulator is one 256-column TMEM region, layer 1 is recomputed
-// per pass (K = 16: 1/16 of the pass's tensor time).
-//
-// warp 0: TMA (W2 [256 x 64] boxes)   warp 1: MMA issuer (warp-uniform, elect)
-// warps 2-9: layer-2 epilogue (2 per TMEM lane quarter, 128 columns each)
-// warps 10-13: X gather + layer-1 drain -> A ring
-constexpr int LT_THREADS = 448;  // 1 TMA + 1 MMA + 8 epilogue + 4 producer warps
-constexpr int LT_SA = 3, LT_SB = 4, LT_XS = 2;
-#ifndef SMLRT_LT_L1B
-#define SMLRT_LT_L1B 4
-#endif
-constexpr int LT_L1B = SMLRT_LT_L1B;  // layer-1 TMEM buffers = MMA lookahead in K chunks
-
-struct LtLay {
-  static constexpr int A_BYTES = GBM * 64 * 2;   // 16 KB
-  static constexpr int B_BYTES = 256 * 64 * 2;   // 32 KB
-  static constexpr int X_BYTES = GBM * 16 * 2;   // 4 KB, SW32
-  static constexpr int OFF_A = 0;
-  static constexpr int OFF_B = OFF_A + LT_SA * A_BYTES;
-  static constexpr int OFF_X = OFF_B + LT_SB * B_BYTES;
-  static constexpr int OFF_W1 = OFF_X + LT_XS * X_BYTES;     // [H1][16] bf16 SW32 (B operand of layer 1)
-  static constexpr int OFF_B1 = OFF_W1 + L12_H1MAX * 32;     // f32 [H1]
-  static constexpr int OFF_B2 = OFF_B1 + L12_H1MAX * 4;      // f32 [H2]
-  static constexpr int OFF_BAR = OFF_B2 + 512 * 4;
-  enum {
-    AFULL = 0, AEMPTY = LT_SA, BFULL = 2 * LT_SA, BEMPTY = BFULL + LT_SB,
-    XFULL = BEMPTY + LT_SB, XEMPTY = XFULL + LT_XS, L1FULL = XEMPTY + LT_XS, L1EMPTY = L1FULL + LT_L1B,
-    TFULL = L1EMPTY + LT_L1B, TEMPTY, NBAR
-  };
-  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
-  static_assert(ALLOC <= 232448, "shared memory budget");
-  static constexpr int T_L2 = 0, T_L1 = 256;  // L2 acc [0,256), L1 buffers of 64 columns from 256
-  static_assert(256 + 64 * LT_L1B <= 512, "TMEM columns");
-};
-
-struct LtArgs {
-  int M, H1, H2, F;
-  int act1, act2;
-  int64_t r0;
-  const __nv_bfloat16* w1p;  // [H1][16] bf16 row-major (K padded with zeros)
-  const float* b1;           // [H1]
-  const float* b2;           // [H2]
-  const void* src;
-  int src_dt;
-  __nv_bfloat16* out;        // [M][H2]
-};
-
-template <int ACT1, int F>
-__device__ __forceinline__ void lt_producer(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int npass,
-                                            const LtArgs& a, const DevPlan& Pin, int q, int lane) {
-  using L = LtLay;
-  const int r = q * 32 + lane;
-  const int KB = a.H1 / 64;
-  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-  const uint32_t abase = smem_u32(smem + L::OFF_A) + r * 128;
-  const uint32_t b1s = smem_u32(smem + L::OFF_B1);
-  auto load_x = [&](int i, float (&x)[F]) {
-    const int u = blockIdx.x + i * gridDim.x;
-    const int64_t m = (int64_t)(u / npass) * GBM + r;
-#pragma unroll
-    for (int f = 0; f < F; ++f) x[f] = 0.0f;
-    if (i < n_my && m < a.M) {
-      const int64_t ro = row_offset_uniform(Pin, (uint32_t)(a.r0 + m));
-#pragma unroll
-      for (int f = 0; f < F; ++f)
-        if (f < a.F) {
-          const int64_t addr = Pin.col_inl[f] + ro;
-          x[f] = a.src_dt == SMLRT_F32 ? __ldg(reinterpret_cast<const float*>(a.src) + addr)
-                                       : __double2float_rn(__ldg(reinterpret_cast<const double*>(a.src) + addr));
-        }
-    }
-  };
-  // X tile of unit i (bf16, SW32 [128 x 16], features >= F zero); unit i+1's
-  // tile is written halfway through unit i so the next unit's first layer-1
-  // MMA never waits on it
-  auto write_x = [&](int i, const float (&xn)[F]) {
-    const int xs = i % LT_XS;
-    mbar_wait(bar + L::XEMPTY + xs, ((i / LT_XS) & 1) ^ 1);
-    float xv[16];
-#pragma unroll
-    for (int f = 0; f < 16; ++f) xv[f] = f < F ? xn[f] : 0.0f;
-    const uint32_t xb = smem_u32(smem + L::OFF_X + xs * L::X_BYTES);
-    st_shared_v4(xb + sw32_offset(r, 0), pack_bf16(xv[0], xv[1]), pack_bf16(xv[2], xv[3]), pack_bf16(xv[4], xv[5]),
-                 pack_bf16(xv[6], xv[7]));
-    st_shared_v4(xb + sw32_offset(r, 8), pack_bf16(xv[8], xv[9]), pack_bf16(xv[10], xv[11]),
-                 pack_bf16(xv[12], xv[13]), pack_bf16(xv[14], xv[15]));
-    fence_async_smem();
-    mbar_arrive(bar + L::XFULL + xs);
-  };
-  float xn[F];
-  load_x(0, xn);
-  if (n_my > 0) write_x(0, xn);
-  load_x(1, xn);
-  int g = 0;  // global K-chunk counter (rings)
-  for (int i = 0; i < n_my; ++i) {
-    for (int kb = 0; kb < KB; ++kb, ++g) {
-      const int lb = g % LT_L1B;
-      mbar_wait(bar + L::L1FULL + lb, (g / LT_L1B) & 1);
-      tc_fence_after();
-      uint32_t v[64];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tmem_ld16(tbase + lane_off + L::T_L1 + lb * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar + L::L1EMPTY + lb);
-      const int sa = g % LT_SA;
-      mbar_wait(bar + L::AEMPTY + sa, ((g / LT_SA) & 1) ^ 1);
-      const uint32_t ab = abase + sa * L::A_BYTES;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {  // 16-byte chunk j: hidden units kb*64 + 8j .. +7
-        const float4 bb0 = ld_shared_f4(b1s + (kb * 64 + 8 * j) * 4);
-        const float4 bb1 = ld_shared_f4(b1s + (kb * 64 + 8 * j + 4) * 4);
-        const float* f = reinterpret_cast<const float*>(v + 8 * j);
-        st_shared_v4(ab + ((j ^ (r & 7)) << 4), act_pack2<ACT1>(f2pk(f[0] + bb0.x, f[1] + bb0.y)),
-                     act_pack2<ACT1>(f2pk(f[2] + bb0.z, f[3] + bb0.w)), act_pack2<ACT1>(f2pk(f[4] + bb1.x, f[5] + bb1.y)),
-                     act_pack2<ACT1>(f2pk(f[6] + bb1.z, f[7] + bb1.w)));
-      }
-      fence_async_smem();
-      mbar_arrive(bar + L::AFULL + sa);
-      if (kb == KB / 2 && i + 1 < n_my) {
-        write_x(i + 1, xn);
-        load_x(i + 2, xn);
-      }
-    }
-  }
-}
-
-template <int ACT2>
-__device__ __forceinline__ void lt_epilogue(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int npass,
-                                            const LtArgs& a, int q, int half, int lane) {
-  using L = LtLay;
-  const int r = q * 32 + lane;
-  const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L2 + half * 128;
-  const uint32_t b2s = smem_u32(smem + L::OFF_B2);
-  for (int i = 0; i < n_my; ++i) {
-    const int u = blockIdx.x + i * gridDim.x;
-    const int64_t m = (int64_t)(u / npass) * GBM + r;
-    const int p = u % npass;
-    w4_wait(bar + L::TFULL, i & 1);
-    tc_fence_after();
-    uint4* o = reinterpret_cast<uint4*>(a.out + m * a.H2 + p * 256 + half * 128);
-    uint32_t v[2][16];
-    tmem_ld16(taddr, v[0]);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      tmem_wait_ld16(v[c & 1]);
-      if (c + 1 < 8) {
-        tmem_ld16(taddr + (c + 1) * 16, v[(c + 1) & 1]);
-      } else {
-        tc_fence_before();
-        mbar_arrive(bar + L::TEMPTY);
-      }
-      uint32_t pk[8];
-#pragma unroll
-      for (int e4 = 0; e4 < 4; ++e4) {
-        const float4 bb = ld_shared_f4(b2s + (p * 256 + half * 128 + c * 16 + 4 * e4) * 4);
-        const uint32_t* vv = v[c & 1] + 4 * e4;
-        pk[2 * e4] = pack_bf16(act_g<ACT2>(__uint_as_float(vv[0]) + bb.x), act_g<ACT2>(__uint_as_float(vv[1]) + bb.y));
-        pk[2 * e4 + 1] =
-            pack_bf16(act_g<ACT2>(__uint_as_float(vv[2]) + bb.z), act_g<ACT2>(__uint_as_float(vv[3]) + bb.w));
-      }
-      if (m < a.M) {
-        o[2 * c] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        o[2 * c + 1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-  }
-}
-
-template <int F>
-__global__ void __launch_bounds__(LT_THREADS, 1)
-    l12tc_kernel(const __grid_constant__ CUtensorMap tb, const __grid_constant__ LtArgs a,
-                 const __grid_constant__ DevPlan Pin) {
-  using L = LtLay;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
-  const int npass = a.H2 / 256;
-  const int n_units = ((a.M + GBM - 1) / GBM) * npass;
-  const int n_my = (int)blockIdx.x < n_units ? (n_units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  const int KB = a.H1 / 64;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < LT_SA; ++i) {
-      mbar_init(bar + L::AFULL + i, 128);
-      mbar_init(bar + L::AEMPTY + i, 1);
-    }
-    for (int i = 0; i < LT_SB; ++i) {
-      mbar_init(bar + L::BFULL + i, 1);
-      mbar_init(bar + L::BEMPTY + i, 1);
-    }
-    for (int i = 0; i < LT_XS; ++i) {
-      mbar_init(bar + L::XFULL + i, 128);
-      mbar_init(bar + L::XEMPTY + i, 1);
-    }
-    for (int i = 0; i < LT_L1B; ++i) {
-      mbar_init(bar + L::L1FULL + i, 1);
-      mbar_init(bar + L::L1EMPTY + i, 128);
-    }
-    mbar_init(bar + L::TFULL, 1);
-    mbar_init(bar + L::TEMPTY, 256);
-    mbar_fence_init();
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
-  }
-  {  // W1 -> SW32 [H1][16] (two 16-byte chunks per row), b1, b2
-    const uint4* g = reinterpret_cast<const uint4*>(a.w1p);
-    for (int i = threadIdx.x; i < a.H1 * 2; i += LT_THREADS) {
-      const int row = i >> 1, ch = i & 1;
-      *reinterpret_cast<uint4*>(smem + L::OFF_W1 + sw32_offset(row, ch * 8)) = g[i];
-    }
-    for (int i = threadIdx.x; i < a.H1; i += LT_THREADS) reinterpret_cast<float*>(smem + L::OFF_B1)[i] = a.b1[i];
-    for (int i = threadIdx.x; i < a.H2; i += LT_THREADS) reinterpret_cast<float*>(smem + L::OFF_B2)[i] = a.b2[i];
-  }
-  fence_async_smem();
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int g = 0;
-      for (int i = 0; i < n_my; ++i) {
-        const int p = (blockIdx.x + i * gridDim.x) % npass;
-        for (int kb = 0; kb < KB; ++kb, ++g) {
-          const int sb = g % LT_SB;
-          w4_wait(bar + L::BEMPTY + sb, ((g / LT_SB) & 1) ^ 1);
-          mbar_expect_tx(bar + L::BFULL + sb, L::B_BYTES);
-          tma_load_2d(smem_u32(smem + L::OFF_B + sb * L::B_BYTES), &tb, bar + L::BFULL + sb, kb * 64, p * 256);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc1 = idesc_bf16(GBM, 64);
-    constexpr uint32_t idesc2 = idesc_bf16(GBM, 256);
-    const uint64_t x0 = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
-    const uint64_t w10 = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
-    const uint64_t a0 = smem_desc(smem_u32(smem + L::OFF_A), 1024, kSwizzle128);
-    const uint64_t b0 = smem_desc(smem_u32(smem + L::OFF_B), 1024, kSwizzle128);
-    auto l1 = [&](int i, int kb, int gg) {  // layer-1 chunk kb of unit i -> L1 buffer gg % LT_L1B
-      const int lb = gg % LT_L1B;
-      mbar_wait(bar + L::L1EMPTY + lb, ((gg / LT_L1B) & 1) ^ 1);
-      tc_fence_after();
-      mma_ss_elect(tbase + L::T_L1 + lb * 64, x0 + (((i % LT_XS) * L::X_BYTES) >> 4),
-                   w10 + ((kb * 64 * 32) >> 4), idesc1, 0);
-      mma_commit_elect(bar + L::L1FULL + lb);
-    };
-    int g = 0;
-    for (int i = 0; i < n_my; ++i) {
-      const int xs = i % LT_XS;
-      mbar_wait(bar + L::XFULL + xs, (i / LT_XS) & 1);
-      for (int j = 0; j < LT_L1B && j < KB; ++j) l1(i, j, g + j);
-      mbar_wait(bar + L::TEMPTY, (i & 1) ^ 1);
-      for (int kb = 0; kb < KB; ++kb, ++g) {
-        const int sa = g % LT_SA, sb = g % LT_SB;
-        mbar_wait(bar + L::AFULL + sa, (g / LT_SA) & 1);
-        mbar_wait(bar + L::BFULL + sb, (g / LT_SB) & 1);
-        tc_fence_after();
-        const uint64_t ad = a0 + ((sa * L::A_BYTES) >> 4), bd = b0 + ((sb * L::B_BYTES) >> 4);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) mma_ss_elect(tbase + L::T_L2, ad + k * 2, bd + k * 2, idesc2, (kb | k) != 0);
-        mma_commit_elect(bar + L::AEMPTY + sa);
-        mma_commit_elect(bar + L::BEMPTY + sb);
-        if (kb + LT_L1B < KB) l1(i, kb + LT_L1B, g + LT_L1B);
-        if (kb == KB - 1) mma_commit_elect(bar + L::XEMPTY + xs);
-      }
-      mma_commit_elect(bar + L::TFULL);
-    }
-    __syncwarp();
-  } else if (warp < 10) {
-    const int q = warp & 3, half = (warp - 2) >> 2;
-    if (a.act2 == SMLRT_RELU)
-      lt_epilogue<SMLRT_RELU>(smem, bar, tbase, n_my, npass, a, q, half, lane);
-    else if (a.act2 == SMLRT_TANH)
-      lt_epilogue<SMLRT_TANH>(smem, bar, tbase, n_my, npass, a, q, half, lane);
-    else
-      lt_epilogue<SMLRT_IDENTITY>(smem, bar, tbase, n_my, npass, a, q, half, lane);
-  } else {
-    const int q = warp & 3;
-    if (a.act1 == SMLRT_RELU)
-      lt_producer<SMLRT_RELU, F>(smem, bar, tbase, n_my, npass, a, Pin, q, lane);
-    else if (a.act1 == SMLRT_TANH)
-      lt_producer<SMLRT_TANH, F>(smem, bar, tbase, n_my, npass, a, Pin, q, lane);
-    else
-      lt_producer<SMLRT_IDENTITY, F>(smem, bar, tbase, n_my, npass, a, Pin, q, lane);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tbase, 512);
-  }
-}
 
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1675,36 +1370,6 @@ int wide_pack(smlrt_model_s& m) {
   return SMLRT_OK;
 }
 
-template <int F>
-int lt_launch(const CUtensorMap& tb, const LtArgs& a, const DevPlan& in, cudaStream_t s) {
-  static int configured = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!(configured & (1 << dev))) {
-    SMLRT_CUDA(cudaFuncSetAttribute(l12tc_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, LtLay::ALLOC));
-    configured |= 1 << dev;
-  }
-  const int units = ((a.M + GBM - 1) / GBM) * (a.H2 / 256);
-  const int grid = std::max(1, std::min(units, sm_count()));
-  l12tc_kernel<F><<<grid, LT_THREADS, LtLay::ALLOC, s>>>(tb, a, in);
-  count_launch();
-  SMLRT_CUDA(cudaGetLastError());
-  return SMLRT_OK;
-}
-
-// SMLRT_WIDE_L1=tc: layer 1 on tcgen05 (l12tc_kernel) instead of the CUDA
-// cores (l12_fused_kernel, default).  Measured on B200, 1M-row blocks:
-// CUDA-core layer 1 1.07 ms, tcgen05 layer 1 1.48-1.55 ms (2 or 4 layer-1
-// TMEM buffers, 4 or 8 epilogue warps) -- the per-unit chain through the
-// layer-1 drain costs more than the CUDA-core FFMAs it removes.
-bool l1_on_cores() {
-  static const int v = [] {
-    const char* e = std::getenv("SMLRT_WIDE_L1");
-    return (e && std::strcmp(e, "tc") == 0) ? 0 : 1;
-  }();
-  return v != 0;
-}
-
 template <int NH, int F>
 int l12_launch(const CUtensorMap& tb, const L12Args& a, const DevPlan& in, cudaStream_t s) {
   using L = L12Lay<NH>;
@@ -1874,23 +1539,7 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
       la.src = in_ptrs[in.uarray];
       la.src_dt = in_dt[in.uarray];
       la.out = a2;
-      if (!l1_on_cores()) {
-        LtArgs lt{};
-        lt.M = n;
-        lt.H1 = h1;
-        lt.H2 = h2;
-        lt.F = F;
-        lt.act1 = m.layers[0].act;
-        lt.act2 = m.layers[1].act;
-        lt.r0 = r;
-        lt.w1p = W1p;
-        lt.b1 = m.layers[0].b;
-        lt.b2 = m.layers[1].b;
-        lt.src = in_ptrs[in.uarray];
-        lt.src_dt = in_dt[in.uarray];
-        lt.out = a2;
-        rc = F <= 6 ? lt_launch<6>(tw2, lt, in, s) : lt_launch<7>(tw2, lt, in, s);
-      } else if (h2 == 512)
+      if (h2 == 512)
         rc = F <= 6 ? l12_launch<2, 6>(tw2, la, in, s) : l12_launch<2, 7>(tw2, la, in, s);
       else
         rc = F <= 6 ? l12_launch<1, 6>(tw2, la, in, s) : l12_launch<1, 7>(tw2, la, in, s);

@@ -835,648 +835,6 @@ __global__ void __launch_bounds__(ss_threads<PAIR>(), 1)
   }
 }
 
-// ============================================================================
-// TS variant (single CTA): the layer-2 A operand never touches shared memory.
-// Layer 1 runs as two N = H1/2 halves into one TMEM region; epilogue 1 drains
-// each half, adds b1, applies the activation, packs bf16 pairs and writes
-// them to TMEM with tcgen05.st; layer 2 then reads A from TMEM (tcgen05.mma
-// with [a-tmem]) and only W2 from shared memory.  Shared-memory traffic per
-// 128-row tile drops from ~230 KB (A2 stores + A2/W2 operand reads) to ~80 KB,
-// which was the binding resource of the SS kernel above.
-//
-// TMEM: L1 half [0, H1/2) | A2 [H1/2, H1): half a = hidden [0, H1/2) at
-// [H1/2, 3H1/4), half b at [3H1/4, H1) (bf16 pairs per 32-bit column) |
-// L2 acc x2 [H1, H1 + 2 H2).  Issue order per tile i (tensor pipe in order):
-//   L2(i) a-half | L1a(i+1) | L2(i) b-half | L1b(i+1)
-// so each L1 half's drain + conversion overlaps half of a layer-2 tile.
-template <int H1, int H2>
-struct LayTS {
-  using B = Lay<H1, H2, 1>;  // weight blob layout (W2 | W1 | ...)
-  static constexpr int KC = H1 / 64;
-  static constexpr int W2_CHUNK = H2 * 128;
-  static constexpr int X_STAGE = BM * 32;
-  static constexpr int OFF_W2 = 0;
-  static constexpr int OFF_W1 = OFF_W2 + KC * W2_CHUNK;  // [H1][16] SW32
-  static constexpr int OFF_X = OFF_W1 + H1 * 32;
-  static constexpr int OFF_W3 = OFF_X + XSTAGES * X_STAGE;  // unused (w3 in params); epilogue2 interface
-  static constexpr int OFF_B3 = OFF_W3;
-  static constexpr int OFF_BAR = OFF_W3 + 16;
-  enum {
-    B_XFULL = 0,
-    B_XEMPTY = XSTAGES,
-    B_L1FULL = 2 * XSTAGES,
-    B_L1EMPTY,
-    B_A2FULL,
-    B_A2EMPTY = B_A2FULL + 2,
-    B_L2FULL = B_A2EMPTY + 2,
-    B_L2EMPTY = B_L2FULL + 2,
-    N_BAR = B_L2EMPTY + 2
-  };
-  static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
-  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
-  static constexpr int T_L1 = 0, T_A2 = H1 / 2, T_L2 = H1;
-  static_assert(H1 + 2 * H2 <= 512, "TMEM columns");
-  static_assert(H1 % 128 == 0, "H1: two halves of a multiple of 64");
-};
-
-// epilogue 1 (TS): warp (q, part) drains columns [part*H1/4, +H1/4) of each
-// L1 half for its 32 rows and writes H1/8 packed columns of A2
-template <int ACT, int H1, int H2>
-__device__ __forceinline__ void epilogue1_ts(uint64_t* bar, uint32_t tbase, int n_my, int part, int q, int lane,
-                                             const TcArgs& a) {
-  using L = LayTS<H1, H2>;
-  constexpr int NC = H1 / 2 / NP;  // fp32 columns per warp per half (64 for H1 = 256, NP = 2)
-  static_assert(NC % 32 == 0, "x32 loads");
-  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-  for (int it = 0; it < n_my; ++it) {
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int u = 2 * it + h;
-      mbar_wait(bar + L::B_L1FULL, u & 1);
-      if (q == 0 && part == 0 && lane == 0) TR(2 + 10 * h, it);
-      tc_fence_after();
-      uint32_t v[NC];
-      if constexpr (NC == 64 && SMLRT_LDX64)
-        tmem_ld64(tbase + lane_off + L::T_L1 + part * NC, *reinterpret_cast<uint32_t(*)[64]>(v));
-      else
-#pragma unroll
-        for (int c = 0; c < NC / 32; ++c)
-          tmem_ld32(tbase + lane_off + L::T_L1 + part * NC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar + L::B_L1EMPTY);
-      // + b1, act, bf16 pairs
-      uint32_t pk[NC / 2];
-      const uint64_t* bp = reinterpret_cast<const uint64_t*>(a.b1 + h * (H1 / 2) + part * NC);
-#pragma unroll
-      for (int e = 0; e < NC / 2; ++e) {
-        const uint64_t sum = add2f(*reinterpret_cast<const uint64_t*>(&v[2 * e]), bp[e]);
-        float lo, hi;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(sum));
-        pk[e] = act_pack<ACT>(lo, hi);
-      }
-      mbar_wait(bar + L::B_A2EMPTY + h, (it & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t dst = tbase + lane_off + L::T_A2 + h * (H1 / 4) + part * (NC / 2);
-#pragma unroll
-      for (int c = 0; c < NC / 32; ++c) tmem_st16(dst + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16 * c));
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar + L::B_A2FULL + h);
-      if (q == 0 && part == 0 && lane == 0) TR(5 + 8 * h, it);
-    }
-  }
-}
-
-template <int H1, int H2>
-__global__ void __launch_bounds__(ss_threads<false>(), 1)
-    mlp3_ts_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
-                   const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
-                   const __grid_constant__ Ptrs8 dst) {
-  using L = LayTS<H1, H2>;
-  using BL = typename L::B;
-  const Sched sc{(int)blockIdx.x, (int)gridDim.x, 0, 0};
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < XSTAGES; ++s) {
-      mbar_init(bar + L::B_XFULL + s, 128);
-      mbar_init(bar + L::B_XEMPTY + s, 1);
-    }
-    mbar_init(bar + L::B_L1FULL, 1);
-    mbar_init(bar + L::B_L1EMPTY, 128 * NP);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar + L::B_A2FULL + b, 128 * NP);
-      mbar_init(bar + L::B_A2EMPTY + b, 1);
-      mbar_init(bar + L::B_L2FULL + b, 1);
-      mbar_init(bar + L::B_L2EMPTY + b, 128);
-    }
-    mbar_fence_init();
-  }
-  if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
-  {  // resident weights: W2 chunks and W1 from the single-CTA blob
-    const int4* g = reinterpret_cast<const int4*>(a.blob);
-    for (int i = threadIdx.x; i < BL::BLOB_W1 / 16; i += ss_threads<false>())
-      reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
-    for (int i = threadIdx.x; i < H1 * 32 / 16; i += ss_threads<false>())
-      reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[BL::BLOB_W1 / 16 + i];
-  }
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-  const int n_my = (a.n_tiles - sc.first + sc.stride - 1) / sc.stride;
-
-  if (warp >= WARP_LOAD && warp < WARP_MMA) {
-    // loader: same X ring as the SS kernel (fast dense path or plan gather)
-    const int t = threadIdx.x - WARP_LOAD * 32;
-    const uint32_t xbase = smem_u32(smem + L::OFF_X);
-    if (a.x_fast != nullptr) {
-      float4 buf[LDEPTH][4];  // LDEPTH tiles of loads in flight (see the SS kernel)
-      auto load_tile = [&](int it, float4(&v)[4]) {
-        const int64_t row0 = a.r0 + sc.tile(it) * BM;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = t + 128 * i;
-          const int64_t row = row0 + (idx >> 2);
-          v[i] = (it < n_my && row < a.r1)
-                     ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      };
-#pragma unroll
-      for (int d = 0; d < LDEPTH; ++d) load_tile(d, buf[d]);
-      for (int it0 = 0; it0 < n_my; it0 += LDEPTH) {
-#pragma unroll
-        for (int d = 0; d < LDEPTH; ++d) {
-          const int it = it0 + d;
-          if (it >= n_my) break;
-          const int s = it % XSTAGES;
-          mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-          const uint32_t xs = xbase + s * L::X_STAGE;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int idx = t + 128 * i;
-            st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(buf[d][i].x, buf[d][i].y),
-                         pack_bf16(buf[d][i].z, buf[d][i].w));
-          }
-          fence_async_smem();
-          mbar_arrive(bar + L::B_XFULL + s);
-          load_tile(it + LDEPTH, buf[d]);
-        }
-      }
-    } else {
-      float cur[16], nxt[16];
-      auto load_row = [&](int it, float(&v)[16]) {
-        const int64_t row = a.r0 + sc.tile(it) * BM + t;
-#pragma unroll
-        for (int f = 0; f < 16; ++f) v[f] = 0.0f;
-        if (row >= a.r1) return;
-        if (Pin.uniform) {
-          const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
-          const void* base = src.p[Pin.uarray];
-          const int dt = src.dt[Pin.uarray];
-#pragma unroll
-          for (int f = 0; f < 16; ++f)
-            if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
-        } else {
-          uint32_t idx[SMLRT_MAX_SWEEP];
-          unravel(Pin, (uint32_t)row, idx);
-#pragma unroll
-          for (int f = 0; f < 16; ++f)
-            if (f < a.F) {
-              const int arr = __ldg(Pin.col_arr + f);
-              v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
-            }
-        }
-      };
-      if (n_my > 0) load_row(0, cur);
-      for (int it = 0; it < n_my; ++it) {
-        if (it + 1 < n_my) load_row(it + 1, nxt);
-        const int s = it % XSTAGES;
-        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-        const uint32_t xs = xbase + s * L::X_STAGE;
-        st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
-                     pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
-        st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
-                     pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
-        fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
-#pragma unroll
-        for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
-      }
-    }
-  } else if (warp == WARP_MMA || (MMA2W && warp == WARP_MMA + 1)) {
-    // whole warp, elect.sync issue (see the SS kernel); with MMA2W layer 1
-    // and layer 2 each have their own issuing warp
-    constexpr uint32_t idesc1 = idesc_bf16(BM, H1 / 2);
-    constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
-    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
-    const uint64_t x0d = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
-    const uint64_t w20d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
-    auto l1 = [&](int it, int h) {
-      const int s = it % XSTAGES, u = 2 * it + h;
-      if (h == 0) mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
-      mbar_wait(bar + L::B_L1EMPTY, (u & 1) ^ 1);
-      if (lane == 0) TR(h == 0 ? 0 : 14, it);
-      tc_fence_after();
-      mma_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d + ((h * (H1 / 2) * 32) >> 4), idesc1, 0);
-      mma_commit_elect(bar + L::B_L1FULL);
-      if (h == 1) mma_commit_elect(bar + L::B_XEMPTY + s);
-    };
-    auto l2 = [&](int it, int h) {
-      const int b = it & 1;
-      if (h == 0) mbar_wait(bar + L::B_L2EMPTY + b, ((it >> 1) & 1) ^ 1);
-      mbar_wait(bar + L::B_A2FULL + h, it & 1);
-      if (lane == 0) TR(h == 0 ? 1 : 15, it);
-      tc_fence_after();
-      const uint32_t d = tbase + L::T_L2 + b * H2;
-#pragma unroll
-      for (int ks = 0; ks < H1 / 32; ++ks) {  // K = 16 steps over this half's H1/2 hidden units
-        const int k = h * (H1 / 2) + ks * 16;
-        mma_ts_elect(d, tbase + L::T_A2 + h * (H1 / 4) + ks * 8,
-                     w20d + (((k / 64) * L::W2_CHUNK + ((k % 64) / 16) * 32) >> 4), idesc2, (h | ks) != 0);
-      }
-      mma_commit_elect(bar + L::B_A2EMPTY + h);
-      if (h == 1) mma_commit_elect(bar + L::B_L2FULL + b);
-    };
-    if (MMA2W && warp == WARP_MMA) {
-      for (int it = 0; it < n_my; ++it) {
-        l1(it, 0);
-        l1(it, 1);
-      }
-    } else if (MMA2W) {
-      for (int it = 0; it < n_my; ++it) {
-        l2(it, 0);
-        l2(it, 1);
-      }
-    } else {
-      if (n_my > 0) {
-        l1(0, 0);
-        l1(0, 1);
-      }
-      for (int it = 0; it < n_my; ++it) {
-        l2(it, 0);
-        if (it + 1 < n_my) l1(it + 1, 0);
-        l2(it, 1);
-        if (it + 1 < n_my) l1(it + 1, 1);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= WARP_EPI1) {
-    const int part = (warp - WARP_EPI1) >> 2;
-    if (a.act1 == SMLRT_RELU)
-      epilogue1_ts<SMLRT_RELU, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
-    else if (a.act1 == SMLRT_TANH)
-      epilogue1_ts<SMLRT_TANH, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
-    else
-      epilogue1_ts<SMLRT_IDENTITY, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
-  } else {
-    if (a.act2 == SMLRT_RELU)
-      epilogue2<SMLRT_RELU, H1, H2, L, false>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
-    else if (a.act2 == SMLRT_TANH)
-      epilogue2<SMLRT_TANH, H1, H2, L, false>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
-    else
-      epilogue2<SMLRT_IDENTITY, H1, H2, L, false>(smem, bar, tbase, n_my, warp, lane, a, Pout, dst, sc);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == WARP_MMA) {
-    tc_fence_after();
-    tmem_dealloc(tbase, 512);
-  }
-}
-
-// ============================================================================
-// TS2 variant: TS (layer-2 A operand in TMEM) with the A2 halves
-// double-buffered by tile parity, so epilogue 1 never waits for layer 2 of
-// the previous tile before refilling A2, and a single layer-2 accumulator
-// drained by 8 epilogue-2 warps (2 per lane quarter, partial dot products
-// combined through shared memory) that release it after two x32 loads.
-// TMEM: L1 half [0, H1/2) | A2 buffer b at H1/2 + b*H1/2 (half a, half b) |
-// L2 acc [3H1/2, 3H1/2 + H2).
-constexpr int T2_EPI2 = 0, T2_EPI1 = 8, T2_LOAD = 16, T2_MMA = 20;
-constexpr int T2_THREADS = (T2_MMA + 1) * 32;
-
-template <int H1, int H2>
-struct LayTS2 {
-  using B = Lay<H1, H2, 1>;  // weight blob layout
-  static constexpr int KC = H1 / 64;
-  static constexpr int W2_CHUNK = H2 * 128;
-  static constexpr int X_STAGE = BM * 32;
-  static constexpr int OFF_W2 = 0;
-  static constexpr int OFF_W1 = OFF_W2 + KC * W2_CHUNK;
-  static constexpr int OFF_X = OFF_W1 + H1 * 32;
-  static constexpr int OFF_RED = OFF_X + XSTAGES * X_STAGE;  // [2][128] f32 partial dots
-  static constexpr int OFF_BAR = OFF_RED + 2 * BM * 4;
-  enum {
-    B_XFULL = 0,
-    B_XEMPTY = XSTAGES,
-    B_L1FULL = 2 * XSTAGES,
-    B_L1EMPTY,
-    B_A2FULL,                // [b*2 + h]
-    B_A2EMPTY = B_A2FULL + 4,
-    B_L2FULL = B_A2EMPTY + 4,
-    B_L2EMPTY,
-    N_BAR
-  };
-  static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
-  static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
-  static constexpr int T_L1 = 0, T_A2 = H1 / 2, T_L2 = H1 / 2 + H1;
-  static_assert(T_L2 + H2 <= 512, "TMEM columns");
-  static_assert(H1 % 128 == 0 && H2 % 64 == 0, "shapes");
-};
-
-template <int ACT, int H1, int H2>
-__device__ __forceinline__ void epilogue1_ts2(uint64_t* bar, uint32_t tbase, int n_my, int part, int q, int lane,
-                                              const TcArgs& a) {
-  using L = LayTS2<H1, H2>;
-  constexpr int NC = H1 / 4;  // fp32 columns per warp per L1 half
-  static_assert(NC % 32 == 0, "x32 loads");
-  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-  for (int it = 0; it < n_my; ++it) {
-    const int b = it & 1;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int u = 2 * it + h;
-      mbar_wait(bar + L::B_L1FULL, u & 1);
-      if (q == 0 && part == 0 && lane == 0) TR(h == 0 ? 2 : 12, it);
-      tc_fence_after();
-      uint32_t v[NC];
-#pragma unroll
-      for (int c = 0; c < NC / 32; ++c)
-        tmem_ld32(tbase + lane_off + L::T_L1 + part * NC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar + L::B_L1EMPTY);
-      uint32_t pk[NC / 2];
-      const uint64_t* bp = reinterpret_cast<const uint64_t*>(a.b1 + h * (H1 / 2) + part * NC);
-#pragma unroll
-      for (int e = 0; e < NC / 2; ++e) {
-        const uint64_t sum = add2f(*reinterpret_cast<const uint64_t*>(&v[2 * e]), bp[e]);
-        float lo, hi;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(sum));
-        pk[e] = act_pack<ACT>(lo, hi);
-      }
-      const int ab = b * 2 + h;
-      mbar_wait(bar + L::B_A2EMPTY + ab, ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t dst = tbase + lane_off + L::T_A2 + b * (H1 / 2) + h * (H1 / 4) + part * (NC / 2);
-#pragma unroll
-      for (int c = 0; c < NC / 32; ++c) tmem_st16(dst + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16 * c));
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar + L::B_A2FULL + ab);
-      if (q == 0 && part == 0 && lane == 0) TR(h == 0 ? 5 : 13, it);
-    }
-  }
-}
-
-template <int ACT, int H1, int H2>
-__device__ __forceinline__ void epilogue2_ts2(uint8_t* smem, uint64_t* bar, uint32_t tbase, int n_my, int part, int q,
-                                              int lane, const TcArgs& a, const DevPlan& Pout, const Ptrs8& dst,
-                                              Sched sc) {
-  using L = LayTS2<H1, H2>;
-  constexpr int NC = H2 / 2;  // columns per warp
-  static_assert(NC % 32 == 0, "x32 loads");
-  const int r = q * 32 + lane;
-  const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + L::T_L2 + part * NC;
-  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);
-  const bool out_fast = Pout.uniform && Pout.n_sweep == 1 && dst.dt[Pout.uarray] == SMLRT_F32 && a.staged == nullptr;
-  float* out_base = out_fast ? reinterpret_cast<float*>(const_cast<void*>(dst.p[Pout.uarray])) + Pout.col_off0
-                             : nullptr;
-  for (int it = 0; it < n_my; ++it) {
-    mbar_wait(bar + L::B_L2FULL, it & 1);
-    if (q == 0 && part == 0 && lane == 0) TR(6, it);
-    tc_fence_after();
-    uint32_t v[NC];
-#pragma unroll
-    for (int c = 0; c < NC / 32; ++c) tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-    tmem_wait_ld();
-    tc_fence_before();
-    mbar_arrive(bar + L::B_L2EMPTY);  // accumulator free: the next tile's layer 2 may start
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int e = 0; e < NC; e += 4) {
-      const int col = part * NC + e;
-      const float4 ww = *reinterpret_cast<const float4*>(a.w3 + col);
-      const float4 bb = *reinterpret_cast<const float4*>(a.b2 + col);
-      acc[((e >> 2) & 1) * 4 + 0] = fmaf(act_t<ACT>(__uint_as_float(v[e]) + bb.x), ww.x, acc[((e >> 2) & 1) * 4 + 0]);
-      acc[((e >> 2) & 1) * 4 + 1] = fmaf(act_t<ACT>(__uint_as_float(v[e + 1]) + bb.y), ww.y, acc[((e >> 2) & 1) * 4 + 1]);
-      acc[((e >> 2) & 1) * 4 + 2] = fmaf(act_t<ACT>(__uint_as_float(v[e + 2]) + bb.z), ww.z, acc[((e >> 2) & 1) * 4 + 2]);
-      acc[((e >> 2) & 1) * 4 + 3] = fmaf(act_t<ACT>(__uint_as_float(v[e + 3]) + bb.w), ww.w, acc[((e >> 2) & 1) * 4 + 3]);
-    }
-    const float partial = ((acc[0] + acc[4]) + (acc[1] + acc[5])) + ((acc[2] + acc[6]) + (acc[3] + acc[7]));
-    float* rb = red + (it & 1) * BM;
-    if (part == 1) rb[r] = partial;
-    // the two warps of lane quarter q meet (named barrier 1 + q, 64 threads)
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-    if (part == 1) continue;
-    if (q == 0 && lane == 0) TR(7, it);
-    const float y = act_f(partial + rb[r] + a.b3, a.act3);
-    const int64_t row = a.r0 + sc.tile(it) * BM + r;
-    bool bad = false;
-    if (row < a.r1) {
-      bad = (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
-      if (out_fast) {
-        out_base[row * Pout.ustride[0]] = y;
-      } else if (a.staged != nullptr) {
-        a.staged[row - a.r0] = y;
-      } else {
-        int64_t addr;
-        int arr;
-        if (Pout.uniform) {
-          addr = Pout.col_off0 + row_offset_uniform(Pout, (uint32_t)row);
-          arr = Pout.uarray;
-        } else {
-          uint32_t idx[SMLRT_MAX_SWEEP];
-          unravel(Pout, (uint32_t)row, idx);
-          addr = col_address(Pout, 0, idx);
-          arr = __ldg(Pout.col_arr);
-        }
-        void* base = const_cast<void*>(dst.p[arr]);
-        if (dst.dt[arr] == SMLRT_F32)
-          reinterpret_cast<float*>(base)[addr] = y;
-        else
-          reinterpret_cast<double*>(base)[addr] = (double)y;
-      }
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(a.status);
-  }
-}
-
-template <int H1, int H2>
-__global__ void __launch_bounds__(T2_THREADS, 1)
-    mlp3_ts2_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ DevPlan Pin,
-                    const __grid_constant__ Ptrs8 src, const __grid_constant__ DevPlan Pout,
-                    const __grid_constant__ Ptrs8 dst) {
-  using L = LayTS2<H1, H2>;
-  using BL = typename L::B;
-  const Sched sc{(int)blockIdx.x, (int)gridDim.x, 0, 0};
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < XSTAGES; ++s) {
-      mbar_init(bar + L::B_XFULL + s, 128);
-      mbar_init(bar + L::B_XEMPTY + s, 1);
-    }
-    mbar_init(bar + L::B_L1FULL, 1);
-    mbar_init(bar + L::B_L1EMPTY, 256);
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(bar + L::B_A2FULL + i, 256);
-      mbar_init(bar + L::B_A2EMPTY + i, 1);
-    }
-    mbar_init(bar + L::B_L2FULL, 1);
-    mbar_init(bar + L::B_L2EMPTY, 256);
-    mbar_fence_init();
-  }
-  if (warp == T2_MMA) tmem_alloc(tmem_slot, 512);
-  {
-    const int4* g = reinterpret_cast<const int4*>(a.blob);
-    for (int i = threadIdx.x; i < BL::BLOB_W1 / 16; i += T2_THREADS)
-      reinterpret_cast<int4*>(smem + L::OFF_W2)[i] = g[i];
-    for (int i = threadIdx.x; i < H1 * 32 / 16; i += T2_THREADS)
-      reinterpret_cast<int4*>(smem + L::OFF_W1)[i] = g[BL::BLOB_W1 / 16 + i];
-  }
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-  const int n_my = (a.n_tiles - sc.first + sc.stride - 1) / sc.stride;
-
-  if (warp >= T2_LOAD && warp < T2_MMA) {
-    const int t = threadIdx.x - T2_LOAD * 32;
-    const uint32_t xbase = smem_u32(smem + L::OFF_X);
-    if (a.x_fast != nullptr) {
-      float4 buf[LDEPTH][4];
-      auto load_tile = [&](int it, float4(&v)[4]) {
-        const int64_t row0 = a.r0 + sc.tile(it) * BM;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = t + 128 * i;
-          const int64_t row = row0 + (idx >> 2);
-          v[i] = (it < n_my && row < a.r1)
-                     ? __ldg(reinterpret_cast<const float4*>(a.x_fast + row * 16) + (idx & 3))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      };
-#pragma unroll
-      for (int d = 0; d < LDEPTH; ++d) load_tile(d, buf[d]);
-      for (int it0 = 0; it0 < n_my; it0 += LDEPTH) {
-#pragma unroll
-        for (int d = 0; d < LDEPTH; ++d) {
-          const int it = it0 + d;
-          if (it >= n_my) break;
-          const int s = it % XSTAGES;
-          mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-          const uint32_t xs = xbase + s * L::X_STAGE;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int idx = t + 128 * i;
-            st_shared_v2(xs + sw32_offset(idx >> 2, (idx & 3) * 4), pack_bf16(buf[d][i].x, buf[d][i].y),
-                         pack_bf16(buf[d][i].z, buf[d][i].w));
-          }
-          fence_async_smem();
-          mbar_arrive(bar + L::B_XFULL + s);
-          load_tile(it + LDEPTH, buf[d]);
-        }
-      }
-    } else {
-      float cur[16], nxt[16];
-      auto load_row = [&](int it, float(&v)[16]) {
-        const int64_t row = a.r0 + sc.tile(it) * BM + t;
-#pragma unroll
-        for (int f = 0; f < 16; ++f) v[f] = 0.0f;
-        if (row >= a.r1) return;
-        if (Pin.uniform) {
-          const int64_t ro = row_offset_uniform(Pin, (uint32_t)row);
-          const void* base = src.p[Pin.uarray];
-          const int dt = src.dt[Pin.uarray];
-#pragma unroll
-          for (int f = 0; f < 16; ++f)
-            if (f < a.F) v[f] = ld_elem(base, dt, __ldg(Pin.col_off + f) + ro);
-        } else {
-          uint32_t idx[SMLRT_MAX_SWEEP];
-          unravel(Pin, (uint32_t)row, idx);
-#pragma unroll
-          for (int f = 0; f < 16; ++f)
-            if (f < a.F) {
-              const int arr = __ldg(Pin.col_arr + f);
-              v[f] = ld_elem(src.p[arr], src.dt[arr], col_address(Pin, f, idx));
-            }
-        }
-      };
-      if (n_my > 0) load_row(0, cur);
-      for (int it = 0; it < n_my; ++it) {
-        if (it + 1 < n_my) load_row(it + 1, nxt);
-        const int s = it % XSTAGES;
-        mbar_wait(bar + L::B_XEMPTY + s, ((it / XSTAGES) & 1) ^ 1);
-        const uint32_t xs = xbase + s * L::X_STAGE;
-        st_shared_v4(xs + sw32_offset(t, 0), pack_bf16(cur[0], cur[1]), pack_bf16(cur[2], cur[3]),
-                     pack_bf16(cur[4], cur[5]), pack_bf16(cur[6], cur[7]));
-        st_shared_v4(xs + sw32_offset(t, 8), pack_bf16(cur[8], cur[9]), pack_bf16(cur[10], cur[11]),
-                     pack_bf16(cur[12], cur[13]), pack_bf16(cur[14], cur[15]));
-        fence_async_smem();
-        mbar_arrive(bar + L::B_XFULL + s);
-#pragma unroll
-        for (int f = 0; f < 16; ++f) cur[f] = nxt[f];
-      }
-    }
-  } else if (warp == T2_MMA) {
-    constexpr uint32_t idesc1 = idesc_bf16(BM, H1 / 2);
-    constexpr uint32_t idesc2 = idesc_bf16(BM, H2);
-    const uint64_t w1d = smem_desc(smem_u32(smem + L::OFF_W1), 256, kSwizzle32);
-    const uint64_t x0d = smem_desc(smem_u32(smem + L::OFF_X), 256, kSwizzle32);
-    const uint64_t w20d = smem_desc(smem_u32(smem + L::OFF_W2), 1024, kSwizzle128);
-    auto l1 = [&](int it, int h) {
-      const int s = it % XSTAGES, u = 2 * it + h;
-      if (h == 0) mbar_wait(bar + L::B_XFULL + s, (it / XSTAGES) & 1);
-      mbar_wait(bar + L::B_L1EMPTY, (u & 1) ^ 1);
-      if (lane == 0) TR(h == 0 ? 0 : 14, it);
-      tc_fence_after();
-      mma_ss_elect(tbase + L::T_L1, x0d + ((s * L::X_STAGE) >> 4), w1d + ((h * (H1 / 2) * 32) >> 4), idesc1, 0);
-      mma_commit_elect(bar + L::B_L1FULL);
-      if (h == 1) mma_commit_elect(bar + L::B_XEMPTY + s);
-    };
-    auto l2 = [&](int it, int h) {
-      const int b = it & 1, ab = b * 2 + h;
-      if (h == 0) mbar_wait(bar + L::B_L2EMPTY, (it & 1) ^ 1);
-      mbar_wait(bar + L::B_A2FULL + ab, (it >> 1) & 1);
-      if (lane == 0) TR(h == 0 ? 1 : 15, it);
-      tc_fence_after();
-#pragma unroll
-      for (int ks = 0; ks < H1 / 32; ++ks) {
-        const int k = h * (H1 / 2) + ks * 16;
-        mma_ts_elect(tbase + L::T_L2, tbase + L::T_A2 + b * (H1 / 2) + h * (H1 / 4) + ks * 8,
-                     w20d + (((k / 64) * L::W2_CHUNK + ((k % 64) / 16) * 32) >> 4), idesc2, (h | ks) != 0);
-      }
-      mma_commit_elect(bar + L::B_A2EMPTY + ab);
-      if (h == 1) mma_commit_elect(bar + L::B_L2FULL);
-    };
-    if (n_my > 0) {
-      l1(0, 0);
-      l1(0, 1);
-    }
-    for (int it = 0; it < n_my; ++it) {
-      l2(it, 0);
-      if (it + 1 < n_my) l1(it + 1, 0);
-      l2(it, 1);
-      if (it + 1 < n_my) l1(it + 1, 1);
-    }
-    __syncwarp();
-  } else if (warp >= T2_EPI1) {
-    const int part = (warp - T2_EPI1) >> 2;
-    if (a.act1 == SMLRT_RELU)
-      epilogue1_ts2<SMLRT_RELU, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
-    else if (a.act1 == SMLRT_TANH)
-      epilogue1_ts2<SMLRT_TANH, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
-    else
-      epilogue1_ts2<SMLRT_IDENTITY, H1, H2>(bar, tbase, n_my, part, warp & 3, lane, a);
-  } else {
-    const int part = warp >> 2;
-    if (a.act2 == SMLRT_RELU)
-      epilogue2_ts2<SMLRT_RELU, H1, H2>(smem, bar, tbase, n_my, part, warp & 3, lane, a, Pout, dst, sc);
-    else if (a.act2 == SMLRT_TANH)
-      epilogue2_ts2<SMLRT_TANH, H1, H2>(smem, bar, tbase, n_my, part, warp & 3, lane, a, Pout, dst, sc);
-    else
-      epilogue2_ts2<SMLRT_IDENTITY, H1, H2>(smem, bar, tbase, n_my, part, warp & 3, lane, a, Pout, dst, sc);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == T2_MMA) {
-    tc_fence_after();
-    tmem_dealloc(tbase, 512);
-  }
-}
-
 // TS self-test: D[128 x N] = A[128 x K] * B[N x K]^T with A staged in TMEM by
 // tcgen05.st (bf16 pairs): validates the TMEM A-operand (TS) layout.
 template <int N>
@@ -1607,29 +965,6 @@ int num_sms() {
   return n;
 }
 
-// SMLRT_TC_KERNEL=ts2: the TS2 kernel (double-buffered TMEM A2, single L2
-// accumulator with 8 epilogue-2 warps)
-bool use_ts2() {
-  static const int v = [] {
-    const char* e = std::getenv("SMLRT_TC_KERNEL");
-    return (e && std::strcmp(e, "ts2") == 0) ? 1 : 0;
-  }();
-  return v != 0;
-}
-
-// SMLRT_TC_KERNEL: "ss" (default: layer-2 A operand in SMEM) or "ts" (A in
-// TMEM).  Measured on B200 (bonds, 16.8M rows): ss 1.13 ms, ts 1.16 ms -- both
-// ~2300-cycle tile periods; the TS kernel's epilogue-1 drain of each L1 half
-// takes ~1000 cycles while layer-2 MMAs run (tools/tc_trace.py), so removing
-// the A2 shared-memory traffic did not shorten the critical loop.
-bool use_ts() {
-  static const int v = [] {
-    const char* e = std::getenv("SMLRT_TC_KERNEL");
-    return (e && std::strcmp(e, "ts") == 0) ? 1 : 0;
-  }();
-  return v != 0;
-}
-
 // CTA-pair kernel (SMLRT_TC_PAIR=1); off by default: measured slower than the
 // single-CTA kernel on bonds (1.24 ms vs 1.14 ms with the elect.sync issuer)
 bool use_pair() {
@@ -1638,12 +973,6 @@ bool use_pair() {
     return e ? std::atoi(e) : 0;
   }();
   return v != 0;
-}
-
-// TS epilogue drains x32 column groups per warp
-template <int H1>
-constexpr bool ts_ok() {
-  return (H1 / 2 / NP) % 32 == 0;
 }
 
 template <int H1, int H2>
@@ -1665,9 +994,6 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
                                     Lay<H1, H2, 1>::ALLOC));
     SMLRT_CUDA(cudaFuncSetAttribute(mlp3_tc_kernel<H1, H2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Lay<H1, H2, 2>::ALLOC));
-    if constexpr (ts_ok<H1>())
-      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      LayTS<H1, H2>::ALLOC));
     configured_mask |= 1 << dev;
   }
   TcArgs a{};
@@ -1706,23 +1032,7 @@ int launch(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs
     const float* base = reinterpret_cast<const float*>(in_ptrs[in.uarray]) + in.col_off0;
     if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) a.x_fast = base;
   }
-  if (!pair && use_ts2()) {
-    static int configured2 = 0;
-    if (!(configured2 & (1 << dev))) {
-      SMLRT_CUDA(cudaFuncSetAttribute(mlp3_ts2_kernel<H1, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      LayTS2<H1, H2>::ALLOC));
-      configured2 |= 1 << dev;
-    }
-    const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-    mlp3_ts2_kernel<H1, H2><<<grid, T2_THREADS, LayTS2<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
-    count_launch();
-  } else if (!pair && use_ts() && ts_ok<H1>()) {
-    if constexpr (ts_ok<H1>()) {
-      const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
-      mlp3_ts_kernel<H1, H2><<<grid, ss_threads<false>(), LayTS<H1, H2>::ALLOC, s>>>(a, in, src, out, dst);
-      count_launch();
-    }
-  } else if (!pair) {
+  if (!pair) {
     const int grid = std::max(1, std::min(a.n_tiles, num_sms()));
     mlp3_tc_kernel<H1, H2, false><<<grid, ss_threads<false>(), Lay<H1, H2, 1>::ALLOC, s>>>(a, in, src, out, dst);
     count_launch();

@@ -138,9 +138,9 @@ def test_bf16_relu_propagates_nan(cuda, tmp_path):
     assert np.isnan(got[1234]) and np.isfinite(np.delete(got, 1234)).all()
 
 
-@pytest.mark.parametrize("env", [{"SMLRT_TC_KERNEL": "ts"}, {"SMLRT_TC_KERNEL": "ts2"}, {"SMLRT_TC_PAIR": "1"}])
+@pytest.mark.parametrize("env", [{"SMLRT_TC_PAIR": "1"}])
 def test_bonds_kernel_variants(cuda, env):
-    """The opt-in bonds kernels (TMEM A operand, TS2, CTA pair) meet the same
+    """The opt-in bonds CTA-pair kernel meets the same
     tolerances; each runs in a subprocess because the switches are read once."""
     import os
     import subprocess
