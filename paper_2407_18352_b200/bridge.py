@@ -37,7 +37,7 @@ __all__ = [
     "ArrayBuffer", "Tensor", "MemoryView", "SliceDescriptor", "ResolvedSlice",
     "extract_symbolic_shape", "resolve_symbolic_shape", "wrap_tensors",
     "compose_tensor", "concretize_to", "scatter_from", "gather_batch",
-    "expected_tensor_shape", "Plan", "build_plan",
+    "expected_tensor_shape", "Plan", "build_plan", "PLAN_CACHE",
 ]
 
 _TORCH = {"f32": torch.float32, "f64": torch.float64}
@@ -327,26 +327,15 @@ def expected_tensor_shape(functor: FunctorDecl, target: MapTarget) -> tuple[int,
 # Plans: wrap_tensors output flattened for the native library
 # ---------------------------------------------------------------------------
 
-class Plan:
-    """Validated, cached native plan over one or more maps.
+class _NativePlan:
+    """Owns one native plan handle; shared by every Plan with the same geometry."""
 
-    `arrays` lists the distinct ArrayBuffers the views address, in the order
-    the native call receives their pointers; `n_cols` is the dense feature
-    width; `n_rows` the flattened sweep size.
-    """
+    __slots__ = ("handle", "n_rows", "n_cols", "__weakref__")
 
-    def __init__(self, handle, arrays, n_rows, n_cols, sweep, direction, views=()):
+    def __init__(self, handle, n_rows, n_cols):
         self.handle = handle
-        self.views = list(views)  # [(array index, MemoryView)]
-        self.arrays = arrays
         self.n_rows = n_rows
         self.n_cols = n_cols
-        self.sweep = sweep
-        self.direction = direction
-
-    def ptrs_and_dtypes(self):
-        return ([a.data.data_ptr() for a in self.arrays],
-                [DTYPE_CODE[a.dtype] for a in self.arrays])
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -358,9 +347,80 @@ class Plan:
             pass
 
 
+class _PlanCache:
+    """Process-wide cache of validated native plans, keyed by geometry only
+    (per view: array index, base offset, shape, element strides; the sweep,
+    the direction and every array's element count).  A native plan holds no
+    pointers -- they are passed per call -- so any Runtime, and the library
+    entry points `concretize_to` / `scatter_from`, reuse one plan (its bounds
+    and injectivity proof included) for every array with that geometry.  The
+    closest reference analogue is the realpath-keyed model cache shared by a
+    Runtime's regions (`runtime.py:185-197`); bounded LRU."""
+
+    def __init__(self, capacity: int = 512):
+        import collections
+        import threading
+        self.capacity = capacity
+        self._d = collections.OrderedDict()
+        self._lock = threading.Lock()
+        self.hits = 0
+        self.misses = 0
+
+    def get(self, key):
+        with self._lock:
+            hit = self._d.get(key)
+            if hit is not None:
+                self._d.move_to_end(key)
+                self.hits += 1
+            return hit
+
+    def put(self, key, plan: _NativePlan):
+        with self._lock:
+            self.misses += 1
+            self._d[key] = plan
+            self._d.move_to_end(key)
+            while len(self._d) > self.capacity:
+                self._d.popitem(last=False)
+
+    def clear(self):
+        with self._lock:
+            self._d.clear()
+
+    def __len__(self):
+        return len(self._d)
+
+
+PLAN_CACHE = _PlanCache()
+
+
+class Plan:
+    """Validated native plan over one or more maps, bound to its arrays.
+
+    `arrays` lists the distinct ArrayBuffers the views address, in the order
+    the native call receives their pointers; `n_cols` is the dense feature
+    width; `n_rows` the flattened sweep size.  The native handle comes from
+    the process-wide PLAN_CACHE.
+    """
+
+    def __init__(self, native, arrays, n_rows, n_cols, sweep, direction, views=()):
+        self._native_plan = native
+        self.handle = native.handle
+        self.views = list(views)  # [(array index, MemoryView)]
+        self.arrays = arrays
+        self.n_rows = n_rows
+        self.n_cols = n_cols
+        self.sweep = sweep
+        self.direction = direction
+
+    def ptrs_and_dtypes(self):
+        return ([a.data.data_ptr() for a in self.arrays],
+                [DTYPE_CODE[a.dtype] for a in self.arrays])
+
+
 def build_plan(view_groups: Sequence[Sequence[MemoryView]], direction: str) -> Plan:
     """Flatten the views of several maps (concatenated on the feature axis,
-    in order) into one native plan.  direction: "to" (gather) | "from" (scatter)."""
+    in order) into one native plan.  direction: "to" (gather) | "from" (scatter).
+    Validation (bounds; injectivity for "from") runs once per geometry."""
     arrays: list[ArrayBuffer] = []
     index: dict[int, int] = {}
     flat = []
@@ -377,9 +437,15 @@ def build_plan(view_groups: Sequence[Sequence[MemoryView]], direction: str) -> P
                 index[key] = len(arrays)
                 arrays.append(v.source)
             flat.append((index[key], v))
-    handle, n_rows, n_cols = _native.plan_create(
-        flat, sweep, direction, [a.data.numel() for a in arrays])
-    return Plan(handle, arrays, n_rows, n_cols, sweep, direction, flat)
+    numel = tuple(a.data.numel() for a in arrays)
+    key = (direction, tuple(sweep) if sweep is not None else None, numel,
+           tuple((a, v.base_offset, tuple(v.shape), tuple(v.strides), v.n_sweep) for a, v in flat))
+    native = PLAN_CACHE.get(key)
+    if native is None:
+        handle, n_rows, n_cols = _native.plan_create(flat, sweep, direction, list(numel))
+        native = _NativePlan(handle, n_rows, n_cols)
+        PLAN_CACHE.put(key, native)
+    return Plan(native, arrays, native.n_rows, native.n_cols, sweep, direction, flat)
 
 
 def _views_for(functor: FunctorDecl, target: MapTarget, array: ArrayBuffer):

@@ -109,3 +109,28 @@ def test_plan_row_ranges():
     p = plan("f: [k, 0:5] = ([k, 0:5])", [(0, 10)], (10, 5), "to")
     with pytest.raises(ValueError):
         _native.plan_row_ranges(p.handle, 5, 11)
+
+
+def test_plan_cache_shared_by_geometry():
+    """One native plan per geometry, process-wide: two arrays (two Runtimes'
+    bindings) with the same shape reuse the validated handle; another
+    geometry or direction gets its own."""
+    from paper_2407_18352_b200.bridge import PLAN_CACHE
+    f = parse_functor_decl("f: [k, 0:5] = ([k, 0:5])")
+    t = MapTarget("a", (ConcreteSlice(0, 700),))
+    p1 = build_plan([_views_for(f, t, cpu_array((700, 5)))], "to")
+    hits = PLAN_CACHE.hits
+    a2 = cpu_array((700, 5))
+    p2 = build_plan([_views_for(f, t, a2)], "to")
+    assert PLAN_CACHE.hits == hits + 1
+    assert p2.handle.value == p1.handle.value and p2.arrays[0] is a2
+    p3 = build_plan([_views_for(f, t, cpu_array((701, 5)))], "to")  # other extent
+    assert p3.handle.value != p1.handle.value
+    g = parse_functor_decl("g: [k, 0:1] = ([k, 0])")
+    p4 = build_plan([_views_for(g, t, cpu_array((700, 5)))], "from")
+    assert p4.handle.value not in (p1.handle.value, p3.handle.value)
+    # errors are not cached: the same bad geometry raises every time
+    bad = MemoryView(cpu_array((64,)), 0, (4, 3, 1), (2, 3, 1), 2)
+    for _ in range(2):
+        with pytest.raises(errors.NonInjectiveScatterError):
+            build_plan([[bad]], "from")
