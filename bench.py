@@ -49,7 +49,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-ALL_CONFIGS = ["options", "bonds", "minibude", "particlefilter", "miniweather"]
+ALL_CONFIGS = ["options", "bonds", "minibude", "particlefilter", "particlefilter_bf16", "miniweather"]
 DEFAULT_CONFIG = "minibude"  # the largest single-GPU config (BASELINE.json configs[2])
 METRIC = "ml(infer) region elements/sec"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -57,8 +57,10 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 # CPU baseline samples (first sweep rows): all-cores
 # variant / as-shipped one-process variant
 CPU_SAMPLE = {"options": 1_000_000, "bonds": 262_144, "minibude": 16_384, "particlefilter": 2_048,
+              "particlefilter_bf16": 2_048,
               "miniweather": 4094 * 2046}
 CPU_SAMPLE_1P = {"options": 250_000, "bonds": 16_384, "minibude": 1_024, "particlefilter": 256,
+                 "particlefilter_bf16": 256,
                  "miniweather": 512 * 2046}
 
 
@@ -211,7 +213,7 @@ def _oracle_rows(wl, r0, r1, out=None):
     fi, fo, ti, to = wl.functors()
     src = wl.arrays[ti.array]
     dst = out if out is not None else wl.arrays[to.array].copy()
-    if wl.spec.name == "particlefilter":
+    if wl.spec.cnn:
         x = oracle.gather(fi, _sub_target(ti, r0, r1), src.reshape(-1), src.shape, _strides(src))
         y, _ = oracle.cnn_forward(wl.layers, x.reshape(r1 - r0, -1), (1, 128, 128))
         oracle.scatter(fo, _sub_target(to, r0, r1), y, dst.reshape(-1), dst.shape, _strides(dst))
@@ -305,7 +307,7 @@ def parity(wl, out_host, rows: int, band: int = 512):
         r1 = min(rows, r0 + band)
         x = oracle.gather(fi, _sub_target(ti, r0, r1), src.reshape(-1), src.shape, _strides(src))
         x = x.reshape(-1, fi.feature_count)
-        if wl.spec.name == "particlefilter":
+        if wl.spec.cnn:
             y, _ = oracle.cnn_forward(wl.layers, x, (1, 128, 128))
         else:
             y, _ = c_oracle.mlp_f32(wl.layers, x)
@@ -438,7 +440,7 @@ def measure(name, args, rank, world, local, dev, headline, pk, pk_src, fp32_peak
         rt.invoke_region(h)
     torch.cuda.synchronize()
     rt.time_kernels = False
-    k_ms = statistics.mean(a.elapsed_time(b) for a, b in rt.kernel_events)
+    k_ms = statistics.mean(rt.kernel_times())
     ms_per_step = max_over_ranks(ms_steps, world, dev) / steps
     total_elems = wl.elements if strong else world * wl.elements
     my_elems = wl.elements
@@ -554,7 +556,7 @@ def measure_halo(args, rank, world, local, dev, headline, pk, pk_src, fp32_peak,
         stepper.step()
     torch.cuda.synchronize()
     rt.time_kernels = False
-    k_ms = statistics.mean(a.elapsed_time(b) for a, b in rt.kernel_events)
+    k_ms = statistics.mean(rt.kernel_times())
     my_elems = slab.rows * (state.shape[2] - 2)
     res = {"workload": spec.name, "value": round(wl.elements / (ms_per_step / 1e3), 1),
            "ms_per_step": round(ms_per_step, 4), "elements": wl.elements, "elements_per_gpu": my_elems,

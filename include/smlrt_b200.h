@@ -159,7 +159,8 @@ int smlrt_model_free(smlrt_model_t model);
 /* which kernel region_infer would run: 0 none, 1 fused exact (templated),
  * 2 unfused exact, 3 fused tcgen05 bf16 (shape-specialised), 4 fused conv
  * front + exact dense, 5 generic tcgen05 bf16 layer chain (any dense model),
- * 6 fused exact with runtime dimensions (any small dense MLP) */
+ * 6 fused exact with runtime dimensions (any small dense MLP), 7 conv front
+ * (bf16 features) + tcgen05 bf16 dense chain (CNN at BF16) */
 int smlrt_model_path(smlrt_model_t model, int32_t n_in_cols, int32_t* path);
 
 /* gather_batch / concretize_to (bridge.py:388-395, 457-462): rows
@@ -199,6 +200,31 @@ int smlrt_region_infer(smlrt_plan_t in_plan, const void* const* in_ptrs,
                        smlrt_model_t model, int64_t row_begin,
                        int64_t row_end, int32_t flags, void* workspace,
                        void* stream, uint32_t* d_status);
+
+/*
+ * Prepared region: the steady-state form of smlrt_region_infer for a
+ * device-resident region invoked repeatedly with the same arrays, model and
+ * rows (Runtime.invoke_region, runtime.py:227-277, once per application
+ * step).  Arguments are validated and copied once; with use_graph the
+ * launches are captured into a CUDA graph and every smlrt_region_run is one
+ * graph launch, the stream synchronisation and the status check
+ * (SMLRT_E_NONFINITE as smlrt_region_infer with SMLRT_SYNC_STATUS).
+ * `d_status` is a device word used by the checked commit.  The plans, model
+ * and arrays must outlive the handle.
+ */
+typedef struct smlrt_prepared_s* smlrt_prepared_t;
+int smlrt_region_prepare(smlrt_plan_t in_plan, const void* const* in_ptrs,
+                         const int32_t* in_dtypes, smlrt_plan_t out_plan,
+                         void* const* out_ptrs, const int32_t* out_dtypes,
+                         smlrt_model_t model, int64_t row_begin,
+                         int64_t row_end, int32_t flags, uint32_t* d_status,
+                         int32_t use_graph, smlrt_prepared_t* out);
+int smlrt_region_run(smlrt_prepared_t prepared, void* stream);
+/* the same, with the device time of the launches (CUDA events recorded on
+ * `stream` around them) in *ms -- the bench's kernel-time measurement */
+int smlrt_region_run_timed(smlrt_prepared_t prepared, void* stream, float* ms);
+int smlrt_region_graphed(smlrt_prepared_t prepared, int32_t* graphed);
+int smlrt_region_release(smlrt_prepared_t prepared);
 
 /*
  * ml(collect) snapshot (runtime.py:279-306 feeding srdb.py:163-208): copy a

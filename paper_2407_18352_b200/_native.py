@@ -92,6 +92,12 @@ SIGNATURES = {
     "smlrt_region_workspace": (_I, [_P, _P, _P, _I64, _I32, C.POINTER(C.c_size_t)]),
     "smlrt_region_infer": (_I, [_P, C.POINTER(_P), C.POINTER(_I32), _P, C.POINTER(_P),
                                 C.POINTER(_I32), _P, _I64, _I64, _I32, _P, _P, _P]),
+    "smlrt_region_prepare": (_I, [_P, C.POINTER(_P), C.POINTER(_I32), _P, C.POINTER(_P), C.POINTER(_I32), _P,
+                                  _I64, _I64, _I32, _P, _I32, C.POINTER(_P)]),
+    "smlrt_region_run": (_I, [_P, _P]),
+    "smlrt_region_run_timed": (_I, [_P, _P, C.POINTER(C.c_float)]),
+    "smlrt_region_graphed": (_I, [_P, C.POINTER(_I32)]),
+    "smlrt_region_release": (_I, [_P]),
     "smlrt_collect_async": (_I, [_P, C.c_size_t, _P, _P, _P]),
     "smlrt_collect_wait": (_I, [_P]),
     "smlrt_tc_selftest": (_I, [_I, _I, _P, _P, _P]),
@@ -274,22 +280,57 @@ def region_infer(pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, f
                                     flags, workspace, stream, status_ptr))
 
 
-def prepare_region(pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, flags, status_ptr, *keep):
-    """A region_infer call with its ctypes arguments built once; returns
-    call(stream) -> 1 if the output was non-finite (SMLRT_SYNC_STATUS) else 0.
-    `keep` holds the objects owning the handles (plans) alive."""
-    fn = lib().smlrt_region_infer
-    args = (pin, _arr(_P, in_ptrs), _arr(_I32, in_dts), pout, _arr(_P, out_ptrs), _arr(_I32, out_dts), model,
-            r0, r1, flags, None)
+class PreparedRegion:
+    """A native prepared region (smlrt_region_prepare): the steady-state
+    invoke_region of a device-resident region, replayed as one CUDA graph.
+    `keep` holds the objects owning the plan/model handles alive."""
 
-    def call(stream, _keep=keep):
-        rc = fn(*args, stream, status_ptr)
+    def __init__(self, pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, flags, status_ptr,
+                 *keep, graph: bool = True):
+        self._keep = keep
+        self.handle = None
+        h = _P()
+        _check(lib().smlrt_region_prepare(pin, _arr(_P, in_ptrs), _arr(_I32, in_dts), pout, _arr(_P, out_ptrs),
+                                          _arr(_I32, out_dts), model, r0, r1, flags, status_ptr, int(graph),
+                                          C.byref(h)))
+        self.handle = h
+        self._run = lib().smlrt_region_run
+
+    @property
+    def graphed(self) -> bool:
+        g = _I32(0)
+        _check(lib().smlrt_region_graphed(self.handle, C.byref(g)))
+        return bool(g.value)
+
+    def __call__(self, stream, timing: list | None = None) -> int:
+        """1 if the output was non-finite, else 0 (other errors raise).
+        `timing`: a list that receives the launches' device time in ms."""
+        if timing is not None:
+            ms = C.c_float(0.0)
+            rc = lib().smlrt_region_run_timed(self.handle, stream, C.byref(ms))
+            timing.append(float(ms.value))
+        else:
+            rc = self._run(self.handle, stream)
         if rc == 0:
             return 0
         if rc == 7:  # SMLRT_E_NONFINITE
             return 1
         _check(rc)
-    return call
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        try:  # at interpreter exit the module globals may already be gone
+            if h is not None and _lib is not None:
+                _lib.smlrt_region_release(h)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def prepare_region(pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, flags, status_ptr, *keep,
+                   graph: bool = True) -> PreparedRegion:
+    return PreparedRegion(pin, in_ptrs, in_dts, pout, out_ptrs, out_dts, model, r0, r1, flags, status_ptr,
+                          *keep, graph=graph)
 
 
 def region_workspace(pin, pout, model, rows, flags) -> int:

@@ -169,7 +169,7 @@ extern "C" int smlrt_model_path(smlrt_model_t m, int32_t n_in_cols, int32_t* pat
   DevPlan dummy{};
   *path = 2;
   if (cnn_model(*m)) {
-    *path = 4;
+    *path = m->precision == SMLRT_BF16 ? (m->chain_first > 0 ? 7 : 0) : 4;
   } else if (m->precision == SMLRT_BF16) {
     if (launch_region_tc(*m, dummy, nullptr, nullptr, 0, dummy, nullptr, nullptr, 0, 0, 0, nullptr,
                          0, nullptr, true) == SMLRT_OK)
@@ -384,6 +384,172 @@ static int region_launch(smlrt_plan_t pin, const void* const* in_ptrs, const int
                                status))
       return e;
   }
+  return SMLRT_OK;
+}
+
+// ---------------------------------------------------------------- prepared regions
+// A device-resident region invoked again and again with the same arrays,
+// model and row range (the reference's steady state: one invoke_region per
+// application timestep, runtime.py:227-277): validated once, its launches
+// (scratch allocation, gather/forward/scatter kernels, tensor maps baked into
+// kernel parameters) captured once into a CUDA graph, then replayed -- one
+// cudaGraphLaunch per call instead of the per-launch host work (tables,
+// tensor-map encoding, scratch allocation) that otherwise sits between the
+// caller's stream work and the first kernel.  Capture failures fall back to
+// the direct launches (same kernels).
+struct smlrt_prepared_s {
+  smlrt_plan_t pin = nullptr, pout = nullptr;
+  smlrt_model_t m = nullptr;
+  std::vector<const void*> in_ptrs;
+  std::vector<void*> out_ptrs;
+  std::vector<int32_t> in_dt, out_dt;
+  int64_t r0 = 0, r1 = 0;
+  int32_t flags = 0;
+  uint32_t* status = nullptr;        // checked commit: device status word
+  volatile uint32_t* h_flag = nullptr;  // fused commit: mapped pinned flag
+  uint32_t* d_flag = nullptr;
+  uint32_t* h_status = nullptr;      // checked commit: pinned read-back
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  unsigned long long kernels = 0;    // kernel nodes per replay (launch counter)
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // smlrt_region_run_timed
+  ~smlrt_prepared_s() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (h_flag) cudaFreeHost(const_cast<uint32_t*>(h_flag));
+    if (h_status) cudaFreeHost(h_status);
+  }
+};
+
+namespace {
+// the launches of one prepared call on stream s (no host sync)
+int prepared_enqueue(smlrt_prepared_s& p, cudaStream_t s) {
+  const bool checked = p.flags & SMLRT_COMMIT_CHECKED;
+  uint32_t* st = checked ? p.status : p.d_flag;
+  if (checked) SMLRT_CUDA(cudaMemsetAsync(p.status, 0, sizeof(uint32_t), s));
+  if (int rc = region_launch(p.pin, p.in_ptrs.data(), p.in_dt.data(), p.pout, p.out_ptrs.data(), p.out_dt.data(),
+                             p.m, p.r0, p.r1, p.flags & ~SMLRT_SYNC_STATUS, nullptr, s, st))
+    return rc;
+  if (checked) SMLRT_CUDA(cudaMemcpyAsync(p.h_status, p.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  return SMLRT_OK;
+}
+}  // namespace
+
+extern "C" int smlrt_region_prepare(smlrt_plan_t pin, const void* const* in_ptrs, const int32_t* in_dt,
+                                    smlrt_plan_t pout, void* const* out_ptrs, const int32_t* out_dt,
+                                    smlrt_model_t m, int64_t r0, int64_t r1, int32_t flags, uint32_t* d_status,
+                                    int32_t use_graph, smlrt_prepared_t* out) {
+  if (!pin || !pout || !m || !in_ptrs || !out_ptrs || !in_dt || !out_dt || !d_status || !out)
+    return fail(SMLRT_E_INVALID, "region_prepare: null argument");
+  if (pin->direction != SMLRT_TO || pout->direction != SMLRT_FROM)
+    return fail(SMLRT_E_INVALID, "region_prepare: plans have the wrong directions");
+  if (pin->n_cols != m->in_features || pout->n_cols != m->out_features || pout->n_rows != pin->n_rows)
+    return fail(SMLRT_E_MODEL_SHAPE, "region_prepare: plans and model disagree (run smlrt_region_infer first)");
+  if (int rc = check_rows(pin, r0, r1)) return rc;
+  int dev = 0;
+  SMLRT_CUDA(cudaGetDevice(&dev));
+  if (dev != m->device) return fail(SMLRT_E_INVALID, "region_prepare: model lives on another device");
+  auto* p = new smlrt_prepared_s();
+  p->pin = pin;
+  p->pout = pout;
+  p->m = m;
+  p->in_ptrs.assign(in_ptrs, in_ptrs + pin->n_arrays);
+  p->out_ptrs.assign(out_ptrs, out_ptrs + pout->n_arrays);
+  p->in_dt.assign(in_dt, in_dt + pin->n_arrays);
+  p->out_dt.assign(out_dt, out_dt + pout->n_arrays);
+  p->r0 = r0;
+  p->r1 = r1;
+  p->flags = flags | SMLRT_SYNC_STATUS;
+  p->status = d_status;
+  auto bail = [&](int rc) {
+    std::string msg = smlrt_last_error();
+    delete p;
+    return fail(rc, msg);
+  };
+  void* hp = nullptr;
+  if (cudaHostAlloc(&hp, sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&p->h_status), sizeof(uint32_t), cudaHostAllocPortable) != cudaSuccess)
+    return bail(fail(SMLRT_E_CUDA, "region_prepare: pinned status allocation failed"));
+  p->h_flag = static_cast<volatile uint32_t*>(hp);
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_flag), hp, 0) != cudaSuccess)
+    return bail(fail(SMLRT_E_CUDA, "region_prepare: mapped status pointer"));
+  if (r1 > r0 && use_graph) {
+    // device tables outside the capture (their first use allocates and copies)
+    DevPlan d;
+    if (int rc = device_tables(pin, &d, in_dt, pin->n_arrays)) return bail(rc);
+    if (int rc = device_tables(pout, &d, out_dt, pout->n_arrays)) return bail(rc);
+    cudaStream_t cs = nullptr;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess) {
+      const unsigned long long n0 = smlrt_launch_count();
+      bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      const int rc = ok ? prepared_enqueue(*p, cs) : SMLRT_E_CUDA;
+      cudaGraph_t g = nullptr;
+      const bool ended = ok && cudaStreamEndCapture(cs, &g) == cudaSuccess && g != nullptr;
+      if (rc == SMLRT_OK && ended && cudaGraphInstantiate(&p->exec, g, 0) == cudaSuccess) {
+        p->graph = g;
+        p->kernels = smlrt_launch_count() - n0;
+        g_launches.fetch_sub(p->kernels, std::memory_order_relaxed);  // captured, not launched
+      } else {
+        if (g) cudaGraphDestroy(g);
+        p->exec = nullptr;
+        g_launches.fetch_sub(smlrt_launch_count() - n0, std::memory_order_relaxed);
+      }
+      cudaGetLastError();  // a refused capture leaves a sticky-free error code behind
+      cudaStreamDestroy(cs);
+    }
+  }
+  *out = p;
+  return SMLRT_OK;
+}
+
+namespace {
+int prepared_run(smlrt_prepared_t p, cudaStream_t s, float* ms) {
+  if (!p) return fail(SMLRT_E_INVALID, "region_run: null handle");
+  if (p->r1 == p->r0) {
+    if (ms) *ms = 0.0f;
+    return SMLRT_OK;
+  }
+  const bool checked = p->flags & SMLRT_COMMIT_CHECKED;
+  *p->h_flag = 0u;
+  if (ms) {
+    for (auto& e : p->ev)
+      if (!e) SMLRT_CUDA(cudaEventCreate(&e));
+    SMLRT_CUDA(cudaEventRecord(p->ev[0], s));
+  }
+  if (p->exec) {
+    SMLRT_CUDA(cudaGraphLaunch(p->exec, s));
+    g_launches.fetch_add(p->kernels, std::memory_order_relaxed);
+  } else if (int rc = prepared_enqueue(*p, s)) {
+    return rc;
+  }
+  if (ms) SMLRT_CUDA(cudaEventRecord(p->ev[1], s));
+  SMLRT_CUDA(cudaStreamSynchronize(s));
+  if (ms) SMLRT_CUDA(cudaEventElapsedTime(ms, p->ev[0], p->ev[1]));
+  const uint32_t st = checked ? *p->h_status : *p->h_flag;
+  if (st & SMLRT_STATUS_NONFINITE) return fail(SMLRT_E_NONFINITE, "forward pass produced NaN/inf");
+  return SMLRT_OK;
+}
+}  // namespace
+
+extern "C" int smlrt_region_run(smlrt_prepared_t p, void* stream) {
+  return prepared_run(p, (cudaStream_t)stream, nullptr);
+}
+
+extern "C" int smlrt_region_run_timed(smlrt_prepared_t p, void* stream, float* ms) {
+  if (!ms) return fail(SMLRT_E_INVALID, "region_run_timed: null ms");
+  return prepared_run(p, (cudaStream_t)stream, ms);
+}
+
+extern "C" int smlrt_region_graphed(smlrt_prepared_t p, int32_t* graphed) {
+  if (!p || !graphed) return fail(SMLRT_E_INVALID, "region_graphed: null argument");
+  *graphed = p->exec != nullptr;
+  return SMLRT_OK;
+}
+
+extern "C" int smlrt_region_release(smlrt_prepared_t p) {
+  delete p;
   return SMLRT_OK;
 }
 

@@ -58,7 +58,19 @@ struct FrontArgs {
   float* out;                  // [rows][out_w]
   const void* src;             // plan array base (window path)
   int src_dt;
+  // bf16 tail (the CNN bf16 path): features as bf16 rows of out_pitch
+  // elements instead of f32 rows in `out`
+  __nv_bfloat16* out_bf;
+  int out_pitch;
 };
+
+// feature i of the front's output row (row - r0)
+__device__ __forceinline__ void put_feat(const FrontArgs& a, int64_t r, int i, float v) {
+  if (a.out_bf != nullptr)
+    a.out_bf[r * a.out_pitch + i] = __float2bfloat16_rn(v);
+  else
+    a.out[r * a.out_w + i] = v;
+}
 
 constexpr int kMaxOC = 16;
 
@@ -112,9 +124,9 @@ __global__ void __launch_bounds__(256) conv_front_kernel(const __grid_constant__
       if (o < a.OC) conv[o * npos + p] = act_exact(__fadd_rn(acc[o], __ldg(a.b + o)), a.act);
   }
   __syncthreads();
-  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  const int64_t orr = row - a.r0;
   if (a.pool <= 1) {
-    for (int i = threadIdx.x; i < a.OC * npos; i += blockDim.x) orow[i] = conv[i];
+    for (int i = threadIdx.x; i < a.OC * npos; i += blockDim.x) put_feat(a, orr, i, conv[i]);
     return;
   }
   const int PH = a.OH / a.pool, PW = a.OW / a.pool;
@@ -124,7 +136,7 @@ __global__ void __launch_bounds__(256) conv_front_kernel(const __grid_constant__
     for (int dy = 0; dy < a.pool; ++dy)
       for (int dx = 0; dx < a.pool; ++dx)
         m = max_nan(m, conv[o * npos + (qy * a.pool + dy) * a.OW + qx * a.pool + dx]);
-    orow[i] = m;
+    put_feat(a, orr, i, m);
   }
 }
 
@@ -185,9 +197,9 @@ __global__ void __launch_bounds__(256) conv_front_fixed_kernel(const __grid_cons
     for (int o = 0; o < OC; ++o) conv[o * npos + p] = act_exact(__fadd_rn(acc[o], __ldg(a.b + o)), a.act);
   }
   __syncthreads();
-  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  const int64_t orr = row - a.r0;
   if (a.pool <= 1) {
-    for (int i = threadIdx.x; i < OC * npos; i += blockDim.x) orow[i] = conv[i];
+    for (int i = threadIdx.x; i < OC * npos; i += blockDim.x) put_feat(a, orr, i, conv[i]);
     return;
   }
   const int PH = a.OH / a.pool, PW = a.OW / a.pool;
@@ -197,7 +209,7 @@ __global__ void __launch_bounds__(256) conv_front_fixed_kernel(const __grid_cons
     for (int dy = 0; dy < a.pool; ++dy)
       for (int dx = 0; dx < a.pool; ++dx)
         m = max_nan(m, conv[o * npos + (qy * a.pool + dy) * a.OW + qx * a.pool + dx]);
-    orow[i] = m;
+    put_feat(a, orr, i, m);
   }
 }
 
@@ -277,7 +289,7 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
     y[2 * op] = act_exact(y[2 * op], a.act);
     y[2 * op + 1] = act_exact(y[2 * op + 1], a.act);
   }
-  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  const int64_t orr = row - a.r0;
   if (a.pool == 2) {
     // 2x2 window = lanes {l, l^1, l^16, l^17}; NaN propagates like np.max
 #pragma unroll
@@ -288,11 +300,11 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
     }
     if (lane < 16 && (lane & 1) == 0) {
 #pragma unroll
-      for (int o = 0; o < 8; ++o) orow[o * 64 + warp * 8 + (lane >> 1)] = y[o];
+      for (int o = 0; o < 8; ++o) put_feat(a, orr, o * 64 + warp * 8 + (lane >> 1), y[o]);
     }
   } else {
 #pragma unroll
-    for (int o = 0; o < 8; ++o) orow[o * 256 + py * 16 + px] = y[o];
+    for (int o = 0; o < 8; ++o) put_feat(a, orr, o * 256 + py * 16 + px, y[o]);
   }
 }
 
@@ -355,7 +367,7 @@ __global__ void __launch_bounds__(256) conv_pool_tma_kernel(const __grid_constan
     y[2 * op] = act_exact(y[2 * op], a.act);
     y[2 * op + 1] = act_exact(y[2 * op + 1], a.act);
   }
-  float* orow = a.out + (row - a.r0) * (int64_t)a.out_w;
+  const int64_t orr = row - a.r0;
   if (a.pool == 2) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
@@ -365,11 +377,11 @@ __global__ void __launch_bounds__(256) conv_pool_tma_kernel(const __grid_constan
     }
     if (lane < 16 && (lane & 1) == 0) {
 #pragma unroll
-      for (int o = 0; o < 8; ++o) orow[o * 64 + warp * 8 + (lane >> 1)] = y[o];
+      for (int o = 0; o < 8; ++o) put_feat(a, orr, o * 64 + warp * 8 + (lane >> 1), y[o]);
     }
   } else {
 #pragma unroll
-    for (int o = 0; o < 8; ++o) orow[o * 256 + py * 16 + px] = y[o];
+    for (int o = 0; o < 8; ++o) put_feat(a, orr, o * 256 + py * 16 + px, y[o]);
   }
 }
 
@@ -508,7 +520,7 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
 
 int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const void* src, int src_dt,
                  int64_t r0, int64_t r1, float* out, int* out_w, int* next_layer, cudaStream_t s,
-                 int64_t src_array_elems = 0) {
+                 int64_t src_array_elems = 0, __nv_bfloat16* out_bf = nullptr, int out_pitch = 0) {
   const DevLayer& c = m.layers[0];
   FrontArgs a{};
   a.x = x;
@@ -528,6 +540,8 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
   a.src = src;
   a.src_dt = src_dt;
   a.pool = 1;
+  a.out_bf = out_bf;
+  a.out_pitch = out_pitch;
   *next_layer = 1;
   if (m.n_layers > 1 && m.layers[1].kind == SMLRT_MAXPOOL2D) {
     a.pool = m.layers[1].kernel;
@@ -692,6 +706,51 @@ cudaStream_t cnn_stream(int dev, int which) {
 }
 }  // namespace
 
+// bf16 CNN region (precision "bf16"): the conv(+pool) front is the exact
+// CUDA-core kernel (it is HBM-bound: its FP32 work fits under the window
+// reads), writing its features as bf16 rows padded to the chain's K; the
+// dense tail (512 -> 128 -> 2 on C4) is the generic tcgen05 layer chain
+// (TMA-fed GEMMs, bias/act/bf16 fused), the f32 outputs go through the
+// out-plan scatter or the checked commit's staging.  The exact path's dense
+// tail was a third of the region on CUDA cores (FP32-bound); on the tensor
+// core it is a few microseconds.
+int launch_region_cnn_bf16(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
+                           const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
+                           int n_out, int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
+  if (m.chain_blob == nullptr || m.chain.empty() || m.chain_first < 1)
+    return fail(SMLRT_E_UNSUPPORTED, "bf16 CNN: the dense tail has a layer wider than 4096");
+  const int64_t rows = r1 - r0;
+  if (rows <= 0) return SMLRT_OK;
+  const int k0 = m.chain[0].k_pad, maxw = chain_max_width(m), G = m.out_features;
+  const int64_t ch = std::min<int64_t>(rows, 1 << 16);
+  const size_t act_bytes = (size_t)ch * maxw * 2;
+  uint8_t* buf;
+  SMLRT_CUDA(cudaMallocAsync(&buf, 2 * act_bytes + (size_t)ch * G * 4, s));
+  auto* act0 = reinterpret_cast<__nv_bfloat16*>(buf);
+  auto* act1 = reinterpret_cast<__nv_bfloat16*>(buf + act_bytes);
+  auto* y = reinterpret_cast<float*>(buf + 2 * act_bytes);
+  int rc = SMLRT_OK;
+  for (int64_t r = r0; r < r1 && !rc; r += ch) {
+    const int64_t n = std::min(ch, r1 - r);
+    // K padding columns must read as zero: the front never writes them and
+    // the chain's ping-pong reuses act0 at another pitch
+    if (m.layers[m.chain_first - 1].out < k0) SMLRT_CUDA(cudaMemsetAsync(act0, 0, (size_t)n * k0 * 2, s));
+    int ow = 0, nl = 0;
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, nullptr, &ow, &nl, s,
+                      in.uarray_numel, act0, k0);
+    if (rc) break;
+    if (nl != m.chain_first) {
+      rc = fail(SMLRT_E_UNSUPPORTED, "bf16 CNN: front and chain disagree on the first dense layer");
+      break;
+    }
+    float* ydst = staged ? staged + (r - r0) * G : y;
+    rc = chain_forward(m, act0, act1, n, ydst, status, s);
+    if (!rc && !staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
+  }
+  cudaFreeAsync(buf, s);
+  return rc;
+}
+
 // Rows are processed in chunks of <= 16384 on the caller's stream.
 // SMLRT_CNN_CHUNKS=k > 1 (experiment, off): k chunks, each with its own
 // feature buffer; the conv fronts (HBM-bound) run in order on a low-priority
@@ -705,6 +764,8 @@ int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* con
                       int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                       int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   if (!in.uniform) return fail(SMLRT_E_UNSUPPORTED, "CNN region needs a single-array input map");
+  if (m.precision == SMLRT_BF16)
+    return launch_region_cnn_bf16(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
   static const int n_chunks = [] {
     const char* e = std::getenv("SMLRT_CNN_CHUNKS");
     const int v = e ? std::atoi(e) : 0;

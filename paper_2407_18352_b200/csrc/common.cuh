@@ -3,6 +3,7 @@
 // sweep unravelling, and error plumbing.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -189,6 +190,7 @@ struct smlrt_model_s {
   };
   std::vector<ChainLayer> chain;
   void* chain_blob = nullptr;
+  int chain_first = -1;  // model layer the chain starts at (CNN: the first dense layer)
   ~smlrt_model_s();
 };
 
@@ -234,7 +236,11 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
                        int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 // generic tcgen05 layer chain (gemm_tc.cu): any dense model, any plans
 bool chain_ok(const smlrt_model_s& m);
+int chain_first_layer(const smlrt_model_s& m);
 int chain_pack(smlrt_model_s& m);
+int chain_max_width(const smlrt_model_s& m);
+int chain_forward(const smlrt_model_s& m, __nv_bfloat16* act0, __nv_bfloat16* act1, int64_t n, float* y,
+                  uint32_t* status, cudaStream_t s);
 int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                         int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                         int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);

@@ -1639,19 +1639,33 @@ int chain_gemm(const void* A, int64_t lda, const void* B, int k_pad, int n_pad, 
 
 }  // namespace
 
-bool chain_ok(const smlrt_model_s& m) {
-  for (const auto& L : m.layers)
-    if (L.kind != SMLRT_DENSE || L.out > 4096) return false;
-  return m.n_layers >= 1;
+// first layer of the chain: 0 for a dense model; for a conv2d(+maxpool2d)
+// model the first dense layer after the front (the CNN bf16 path runs the
+// front on CUDA cores and its dense tail as this chain); -1 if none fits
+int chain_first_layer(const smlrt_model_s& m) {
+  int l = 0;
+  if (cnn_model(m)) l = (m.n_layers > 1 && m.layers[1].kind == SMLRT_MAXPOOL2D) ? 2 : 1;
+  if (l >= m.n_layers) return -1;
+  for (int k = l; k < m.n_layers; ++k)
+    if (m.layers[k].kind != SMLRT_DENSE || m.layers[k].out > 4096) return -1;
+  return l;
 }
 
+bool chain_ok(const smlrt_model_s& m) { return !cnn_model(m) && chain_first_layer(m) == 0; }
+
 int chain_pack(smlrt_model_s& m) {
-  if (!chain_ok(m)) return SMLRT_OK;
+  const int first = chain_first_layer(m);
+  if (first < 0) return SMLRT_OK;
   std::vector<uint8_t> blob;
   const float* p = m.host_params.data();
-  int k = chain_k0(m.in_features);
+  for (int l = 0; l < first; ++l) {  // skip the front's parameters (conv W, b; pooling has none)
+    const auto& L = m.layers[l];
+    if (L.kind == SMLRT_CONV2D) p += (size_t)L.out_c * L.in_c * L.kernel * L.kernel + L.out_c;
+  }
+  int k = chain_k0(m.layers[first].in);
   m.chain.clear();
-  for (int l = 0; l < m.n_layers; ++l) {
+  m.chain_first = first;
+  for (int l = first; l < m.n_layers; ++l) {
     const auto& L = m.layers[l];
     smlrt_model_s::ChainLayer c{};
     c.k_pad = k;
@@ -1674,20 +1688,61 @@ int chain_pack(smlrt_model_s& m) {
   return SMLRT_OK;
 }
 
+int chain_max_width(const smlrt_model_s& m) {
+  int w = m.chain.empty() ? 0 : m.chain[0].k_pad;
+  for (const auto& c : m.chain) w = std::max(w, c.n_pad);
+  return w;
+}
+
+// the chain's GEMMs over n rows whose bf16 layer-0 activations are in act0
+// ([n][k_pad0]); act1 is a second [n][max_width] buffer; the last layer
+// writes f32 [n][G] rows into y
+int chain_forward(const smlrt_model_s& m, __nv_bfloat16* act0, __nv_bfloat16* act1, int64_t n, float* y,
+                  uint32_t* status, cudaStream_t s) {
+  const uint8_t* wb = reinterpret_cast<const uint8_t*>(m.chain_blob);
+  const int G = m.out_features;
+  DevPlan none{};
+  OutPtrs dst{};
+  __nv_bfloat16* cur = act0;
+  __nv_bfloat16* nxt = act1;
+  const int nl = (int)m.chain.size();
+  for (int l = 0; l < nl; ++l) {
+    const auto& c = m.chain[l];
+    GemmArgs g{};
+    g.M = (int)n;
+    g.act = c.act;
+    g.bias = reinterpret_cast<const float*>(wb + c.b_off);
+    g.status = status;
+    const void* W = wb + c.w_off;
+    int rc;
+    if (l + 1 < nl) {
+      g.out = nxt;
+      g.ldo = c.n_pad;
+      rc = chain_gemm<EPI_BF16>(cur, c.k_pad, W, c.k_pad, c.n_pad, g, none, dst, s);
+      std::swap(cur, nxt);
+    } else {
+      g.out_f32 = y;
+      g.ldo = G;
+      g.n_valid = G;
+      rc = chain_gemm<EPI_F32>(cur, c.k_pad, W, c.k_pad, c.n_pad, g, none, dst, s);
+    }
+    if (rc) return rc;
+  }
+  return SMLRT_OK;
+}
+
 int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                         int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                         int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
-  if (m.chain_blob == nullptr || m.chain.empty())
-    return fail(SMLRT_E_UNSUPPORTED, "bf16 layer chain: model has non-dense layers or a layer wider than 4096");
+  if (m.chain_blob == nullptr || m.chain.empty() || m.chain_first != 0)
+    return fail(SMLRT_E_UNSUPPORTED, "bf16 layer chain: model has non-dense or > 4096-wide layers");
   if (n_in > 8 || n_out > 8) return fail(SMLRT_E_UNSUPPORTED, "bf16 layer chain: more than 8 arrays per plan");
   Ptrs src{};
   for (int i = 0; i < n_in; ++i) {
     src.p[i] = in_ptrs[i];
     src.dt[i] = in_dt[i];
   }
-  OutPtrs dst{};
-  int maxw = m.chain[0].k_pad;
-  for (const auto& c : m.chain) maxw = std::max(maxw, c.n_pad);
+  const int maxw = chain_max_width(m);
   const int G = m.out_features;
   // rows per block: two bf16 activation buffers + the f32 output stay within 256 MB
   const int64_t rows = r1 - r0;
@@ -1698,8 +1753,6 @@ int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* c
   auto* act0 = reinterpret_cast<__nv_bfloat16*>(buf);
   auto* act1 = act0 + ch * maxw;
   auto* y = reinterpret_cast<float*>(act1 + ch * maxw);
-  const uint8_t* wb = reinterpret_cast<const uint8_t*>(m.chain_blob);
-  DevPlan none{};
   int rc = SMLRT_OK;
   for (int64_t r = r0; r < r1 && !rc; r += ch) {
     const int64_t n = std::min(ch, r1 - r);
@@ -1711,29 +1764,8 @@ int launch_region_chain(const smlrt_model_s& m, const DevPlan& in, const void* c
       rc = fail(SMLRT_E_CUDA, "chain gather launch failed");
       break;
     }
-    __nv_bfloat16* cur = act0;
-    __nv_bfloat16* nxt = act1;
-    for (int l = 0; l < m.n_layers && !rc; ++l) {
-      const auto& c = m.chain[l];
-      GemmArgs g{};
-      g.M = (int)n;
-      g.act = c.act;
-      g.bias = reinterpret_cast<const float*>(wb + c.b_off);
-      g.status = status;
-      const void* W = wb + c.w_off;
-      if (l + 1 < m.n_layers) {
-        g.out = nxt;
-        g.ldo = c.n_pad;
-        rc = chain_gemm<EPI_BF16>(cur, c.k_pad, W, c.k_pad, c.n_pad, g, none, dst, s);
-        std::swap(cur, nxt);
-      } else {
-        // f32 rows: straight into the checked commit's staging, else a scratch block for the scatter
-        g.out_f32 = staged != nullptr ? staged + (r - r0) * G : y;
-        g.ldo = G;
-        g.n_valid = G;
-        rc = chain_gemm<EPI_F32>(cur, c.k_pad, W, c.k_pad, c.n_pad, g, none, dst, s);
-      }
-    }
+    // f32 rows: straight into the checked commit's staging, else a scratch block for the scatter
+    rc = chain_forward(m, act0, act1, n, staged != nullptr ? staged + (r - r0) * G : y, status, s);
     if (!rc && staged == nullptr)
       rc = launch_scatter(out, y, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
   }

@@ -181,10 +181,13 @@ class Runtime:
                (staged; nothing written if the output is non-finite, the
                reference's error-before-write order, runtime.py:341-344).
     shard:     (rank, world) row block processed by this instance.
+    graphs:    replay the launches of a repeated device-resident region as
+               one CUDA graph (smlrt_region_prepare); default on,
+               SMLRT_GRAPHS=0 turns it off.
     """
 
     def __init__(self, precision: Optional[str] = None, commit: str = "fused",
-                 shard: Optional[tuple[int, int]] = None, device=None):
+                 shard: Optional[tuple[int, int]] = None, device=None, graphs: Optional[bool] = None):
         if commit not in ("fused", "checked"):
             raise ValueError("commit must be 'fused' or 'checked'")
         self._regions: dict[str, RegionDescriptor] = {}
@@ -200,11 +203,13 @@ class Runtime:
         self.precision = precision
         self.commit = commit
         self.shard = shard
+        self.graphs = graphs if graphs is not None else os.environ.get("SMLRT_GRAPHS", "1") != "0"
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
             else None)
         self._status = None
-        # bench/profiling hook: CUDA events around each fused launch, on its stream
+        # bench/profiling hook: device time of each region's launches (CUDA
+        # events on their stream; kernel_times() reads them as ms)
         self.time_kernels = False
         self.kernel_events: list = []
         self._realpaths: dict = {}  # model path -> realpath (the model cache key, runtime.py:186)
@@ -466,7 +471,7 @@ class Runtime:
         if self.device is None:
             raise RuntimeError("no CUDA device: the B200 runtime has no CPU data path")
         fast = self._fast.get(desc.name)
-        if fast is not None and not self.time_kernels and fast[0] == self._fast_key(desc, model):
+        if fast is not None and fast[0] == self._fast_key(desc, model):
             return self._run_prepared(fast[1], st)
         host_in = desc.in_maps + desc.inout_maps
         host_out = desc.out_maps + desc.inout_maps
@@ -513,16 +518,16 @@ class Runtime:
         flags = _native.COMMIT_CHECKED if staged else _native.COMMIT_FUSED
         # device-resident outputs: status reset, launch, status read-back and
         # the stream sync happen inside one native call (SMLRT_SYNC_STATUS)
-        # (kernel timing wants the events around the launches alone: old path)
-        sync_native = not self.time_kernels and all(m.array.is_device for m in host_out)
+        sync_native = all(m.array.is_device for m in host_out)
         if sync_native:
             flags |= _native.SYNC_STATUS
             # device-resident region: later calls with the same arrays, model
-            # and settings skip straight to the native call with these arguments
+            # and settings replay a prepared native call (a CUDA graph of
+            # this call's launches) with these arguments
             if all(m.array.is_device for m in host_in):
                 self._fast[desc.name] = (self._fast_key(desc, model), _native.prepare_region(
                     pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1, flags, status.data_ptr(),
-                    pin, pout, model))
+                    pin, pout, model, graph=self.graphs))
         else:
             status.zero_()
         if self.time_kernels:
@@ -557,9 +562,14 @@ class Runtime:
 
     def _run_prepared(self, call, st) -> RegionOutcome:
         """The steady-state surrogate call: one native call (status reset,
-        fused launch, status read-back, stream sync) with cached arguments."""
+        graph launch, status read-back, stream sync) with cached arguments."""
         t0 = time.perf_counter_ns()
-        bad = call(torch._C._cuda_getCurrentRawStream(self.device.index))
+        if self.time_kernels:
+            ms = []
+            bad = call(torch._C._cuda_getCurrentRawStream(self.device.index), ms)
+            self.kernel_events.append(ms[0])
+        else:
+            bad = call(torch._C._cuda_getCurrentRawStream(self.device.index))
         infer_ns = _ns_since(t0)
         if bad:
             raise NonFiniteOutputError("forward pass produced NaN/inf")
@@ -651,6 +661,12 @@ class Runtime:
         return RegionOutcome(path_taken=SURROGATE, elapsed_region_ns=infer_ns,
                              elapsed_map_to_ns=map_to, elapsed_map_from_ns=0,
                              elapsed_infer_ns=infer_ns)
+
+    def kernel_times(self) -> list:
+        """ms per timed region call (time_kernels): the prepared call measures
+        its own launches; the first call's events are read here."""
+        torch.cuda.synchronize(self.device)
+        return [e if isinstance(e, float) else e[0].elapsed_time(e[1]) for e in self.kernel_events]
 
     def stats(self, handle: str) -> RegionStats:
         self._region(handle)

@@ -43,6 +43,10 @@ class Spec:
     flops: int = 0        # override for non-MLP models
 
     @property
+    def cnn(self) -> bool:
+        return self.name.startswith("particlefilter")
+
+    @property
     def flops_per_elem(self) -> int:
         return self.flops or 2 * sum(a * b for a, b in zip(self.dims, self.dims[1:]))
 
@@ -64,6 +68,12 @@ CONFIGS = {
                            "functor(loc: [k, 0:2] = ([k, 0], [k, 1]))",
                            "map(to: win(frames[0:N]))", "map(from: loc(locs[0:N]))", "hbm", 65_544,
                            flops=393_728),
+    # the same CNN at bf16: exact conv front, dense tail on the tensor core
+    "particlefilter_bf16": Spec("particlefilter_bf16", 16_384, [16384, 512, 128, 2], "bf16",
+                                "functor(win: [k, 0:128, 0:128] = ([k, 16:144, 16:144]))",
+                                "functor(loc: [k, 0:2] = ([k, 0], [k, 1]))",
+                                "map(to: win(frames[0:N]))", "map(from: loc(locs[0:N]))", "hbm", 65_544,
+                                flops=393_728),
     "miniweather": Spec("miniweather", 4094 * 2046, [36, 8, 4], "fp32",
                         "functor(halo: [i, j, 0:4, 0:3, 0:3] = ([0:4, i-1:i+2, j-1:j+2]))",
                         "functor(pts: [i, j, 0:4] = ([0, i, j], [1, i, j], [2, i, j], [3, i, j]))",
@@ -142,11 +152,11 @@ def cnn_layers(seed=0):
 
 def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Workload:
     s = CONFIGS[name]
-    if name == "particlefilter":
+    if s.cnn:
         layers = cnn_layers()
         model = Model(16384, 2, [Conv2dLayer(layers[0][1], layers[0][2], 8, 8, "relu"),
                                  MaxPool2dLayer(2)] + [DenseLayer(w, b, a) for _, w, b, a in layers[2:]],
-                      precision="fp32", input_shape=(1, 128, 128))
+                      precision=s.precision, input_shape=(1, 128, 128))
     else:
         layers = init_weights(s.dims)
         model = Model(s.dims[0], s.dims[-1], [DenseLayer(w, b, a) for w, b, a in layers],
@@ -166,7 +176,7 @@ def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Worklo
         rng = np.random.default_rng(3 + seed_offset)
         poses = (rng.random((6, n), dtype=np.float32) * 2 - 1).astype(np.float32)
         arrays, env = {"poses": poses, "energy": np.zeros(n, np.float32)}, {"N": n}
-    elif name == "particlefilter":
+    elif s.cnn:
         n = elements or s.elements
         rng = np.random.default_rng(4 + seed_offset)
         arrays = {"frames": rng.random((n, 160, 160), dtype=np.float32), "locs": np.zeros((n, 2), np.float32)}
