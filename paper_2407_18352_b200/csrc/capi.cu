@@ -476,7 +476,9 @@ extern "C" int smlrt_region_prepare(smlrt_plan_t pin, const void* const* in_ptrs
   if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_flag), hp, 0) != cudaSuccess)
     return bail(fail(SMLRT_E_CUDA, "region_prepare: mapped status pointer"));
   if (r1 > r0 && use_graph) {
-    // device tables outside the capture (their first use allocates and copies)
+    // device tables and the pool setting outside the capture (their first
+    // use allocates, copies or sets pool attributes: not capturable)
+    warm_pool();
     DevPlan d;
     if (int rc = device_tables(pin, &d, in_dt, pin->n_arrays)) return bail(rc);
     if (int rc = device_tables(pout, &d, out_dt, pout->n_arrays)) return bail(rc);
