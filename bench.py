@@ -49,7 +49,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-ALL_CONFIGS = ["options", "bonds", "minibude", "particlefilter", "particlefilter_bf16", "miniweather"]
+ALL_CONFIGS = ["options", "bonds", "minibude", "particlefilter", "particlefilter_bf16", "miniweather",
+               "miniweather_bf16"]
 DEFAULT_CONFIG = "minibude"  # the largest single-GPU config (BASELINE.json configs[2])
 METRIC = "ml(infer) region elements/sec"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -58,10 +59,10 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 # variant / as-shipped one-process variant
 CPU_SAMPLE = {"options": 1_000_000, "bonds": 262_144, "minibude": 16_384, "particlefilter": 2_048,
               "particlefilter_bf16": 2_048,
-              "miniweather": 4094 * 2046}
+              "miniweather": 4094 * 2046, "miniweather_bf16": 4094 * 2046}
 CPU_SAMPLE_1P = {"options": 250_000, "bonds": 16_384, "minibude": 1_024, "particlefilter": 256,
                  "particlefilter_bf16": 256,
-                 "miniweather": 512 * 2046}
+                 "miniweather": 512 * 2046, "miniweather_bf16": 512 * 2046}
 
 
 def peaks():
@@ -460,7 +461,7 @@ def measure(name, args, rank, world, local, dev, headline, pk, pk_src, fp32_peak
     if rank == 0 and not args.no_parity:
         _, _, _, to = wl.functors()
         out_host = wl.buffers[to.array].to_numpy()
-        n = rows0 if name in ("options", "miniweather") else min(rows0, CPU_SAMPLE[name])
+        n = rows0 if name in ("options", "miniweather", "miniweather_bf16") else min(rows0, CPU_SAMPLE[name])
         if strong:
             n = min(n, _shard_rows(rows0, shard)[1])
         res["parity"] = parity(wl, out_host, n)
@@ -481,9 +482,9 @@ def e2e(wl, args, rank, world, dev, mdir, shard):
     import paper_2407_18352_b200 as sm
     from paper_2407_18352_b200 import workloads
     from paper_2407_18352_b200.runtime import _covers
-    hw = workloads.make(wl.spec.name, wl.elements if wl.spec.name != "miniweather" else None,
-                        seed_offset=0 if shard else rank)
-    if wl.spec.name == "miniweather" and wl.elements != wl.spec.elements:
+    mw = wl.spec.name.startswith("miniweather")
+    hw = workloads.make(wl.spec.name, wl.elements if not mw else None, seed_offset=0 if shard else rank)
+    if mw and wl.elements != wl.spec.elements:
         hw = workloads.make(wl.spec.name, wl.elements, seed_offset=0 if shard else rank)
     hw.to_device(pinned_host=True)
     rt2 = sm.Runtime(device=dev, shard=shard)

@@ -234,6 +234,10 @@ int wide_pack(smlrt_model_s& m);
 int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                        const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
                        int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
+// bf16 halo-stencil regions on tcgen05 (stencil_tc.cu); SMLRT_E_UNSUPPORTED if not that shape
+int launch_region_stencil_tc(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
+                             const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
+                             int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 // generic tcgen05 layer chain (gemm_tc.cu): any dense model, any plans
 bool chain_ok(const smlrt_model_s& m);
 int chain_first_layer(const smlrt_model_s& m);

@@ -1159,7 +1159,9 @@ int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* cons
     return m.precision == SMLRT_BF16 && (shape_is(m, 256, 128) || shape_is(m, 128, 64) || wide_shape(m))
                ? SMLRT_OK
                : SMLRT_E_UNSUPPORTED;
-  int rc = SMLRT_E_UNSUPPORTED;
+  // halo stencils over a 2-D sweep (C5 shape): the plan decides, not the model alone
+  int rc = launch_region_stencil_tc(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, r0, r1, staged, s, status);
+  if (rc != SMLRT_E_UNSUPPORTED) return rc;
   if (m.tc_blob != nullptr) {
     if (wide_shape(m))
       rc = launch_region_wide(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);

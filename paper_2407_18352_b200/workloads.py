@@ -79,6 +79,12 @@ CONFIGS = {
                         "functor(pts: [i, j, 0:4] = ([0, i, j], [1, i, j], [2, i, j], [3, i, j]))",
                         "map(to: halo(state[1:NX-1, 1:NZ-1]))",
                         "map(from: pts(state_new[1:NX-1, 1:NZ-1]))", "hbm", 32),
+    # the same region at bf16: layer 1 on tcgen05 (stencil kernel), HBM-bound
+    "miniweather_bf16": Spec("miniweather_bf16", 4094 * 2046, [36, 8, 4], "bf16",
+                             "functor(halo: [i, j, 0:4, 0:3, 0:3] = ([0:4, i-1:i+2, j-1:j+2]))",
+                             "functor(pts: [i, j, 0:4] = ([0, i, j], [1, i, j], [2, i, j], [3, i, j]))",
+                             "map(to: halo(state[1:NX-1, 1:NZ-1]))",
+                             "map(from: pts(state_new[1:NX-1, 1:NZ-1]))", "hbm", 32),
 }
 
 
@@ -181,7 +187,7 @@ def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Worklo
         rng = np.random.default_rng(4 + seed_offset)
         arrays = {"frames": rng.random((n, 160, 160), dtype=np.float32), "locs": np.zeros((n, 2), np.float32)}
         env = {"N": n}
-    elif name == "miniweather":
+    elif name.startswith("miniweather"):
         nx, nz = (4096, 2048) if elements is None else _grid_for(elements)
         state = np.stack([_bumps(nx, nz, k + seed_offset) for k in range(4)])
         arrays = {"state": state, "state_new": np.zeros_like(state)}
