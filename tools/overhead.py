@@ -36,20 +36,31 @@ def main():
         wl = workloads.make("options", rows)
         wl.to_device()
         sm.save_model(wl.model, os.path.join(tmp, "o"))
-        rt = sm.Runtime()
-        h = rt.register_region(wl.descriptor(os.path.join(tmp, "o")))
-        us = timed(rt, h)
-        prof = None
-        if rows == 1 and os.environ.get("PROFILE"):
-            import cProfile
-            import pstats
-            pr = cProfile.Profile()
-            pr.enable()
+        for graphs in (True, False):
+            rt = sm.Runtime(graphs=graphs)
+            h = rt.register_region(wl.descriptor(os.path.join(tmp, "o")))
+            us = timed(rt, h)
+            # the native prepared call alone (no Python dispatch above it)
+            call = rt._fast["options"][1]
+            stream = torch.cuda.current_stream().cuda_stream
+            t0 = time.perf_counter()
             for _ in range(200):
-                rt.invoke_region(h)
-            pr.disable()
-            pstats.Stats(pr).sort_stats("tottime").print_stats(15)
-        print(json.dumps({"what": "invoke_region wall", "rows": rows, "us_per_call": round(us, 1)}), flush=True)
+                call(stream)
+            native_us = (time.perf_counter() - t0) / 200 * 1e6
+            print(json.dumps({"what": "invoke_region wall", "rows": rows, "graphs": graphs,
+                              "us_per_call": round(us, 1), "native_prepared_us": round(native_us, 1)}), flush=True)
+            if rows == 1 and graphs and os.environ.get("PROFILE"):
+                import cProfile
+                import pstats
+                pr = cProfile.Profile()
+                pr.enable()
+                for _ in range(200):
+                    rt.invoke_region(h)
+                pr.disable()
+                pstats.Stats(pr).sort_stats("tottime").print_stats(12)
+            del rt
+    if os.environ.get("ONLY_FIXED"):
+        return
     # checked vs fused commit per config (step time, CUDA events)
     for name in ("options", "bonds", "minibude", "particlefilter", "miniweather"):
         wl = workloads.make(name)
