@@ -147,6 +147,29 @@ def _shard_rows(n_rows: int, shard) -> tuple[int, int]:
     return min(rank * per, n_rows), min((rank + 1) * per, n_rows)
 
 
+def gather_rows_to_root(local: torch.Tensor, n_rows: int, shard, root: int = 0, group=None):
+    """Concatenate every rank's block of sweep rows (`_shard_rows` order) on
+    `root`: the collect snapshots of a sharded region go to the one rank that
+    holds the SRDB writer lock (srdb.py:116-126), SURVEY.md 8(e).  `local` is
+    this rank's [r1 - r0, F] tile; blocks are padded to the largest so one
+    collective (NCCL send/recv under torch.distributed.gather) moves them.
+    Returns the [n_rows, F] tensor on root, None elsewhere."""
+    import torch.distributed as dist
+    rank, world = shard
+    per = -(-n_rows // world)
+    if dist.get_backend(group) == "gloo" and local.is_cuda:
+        local = local.cpu()  # gloo gathers host tensors (NCCL moves device tensors directly)
+    buf = local
+    if local.shape[0] != per:
+        buf = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        buf[: local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in range(world)] if rank == root else None
+    dist.gather(buf.contiguous(), parts, dst=root, group=group)
+    if rank != root:
+        return None
+    return torch.cat(parts)[:n_rows]
+
+
 class _Staging:
     """Device mirrors of host-resident ArrayBuffers (the e2e path)."""
 
@@ -184,10 +207,14 @@ class Runtime:
     graphs:    replay the launches of a repeated device-resident region as
                one CUDA graph (smlrt_region_prepare); default on,
                SMLRT_GRAPHS=0 turns it off.
+    collect_root: with `shard` and an initialised torch.distributed group,
+               ml(collect) snapshots each rank's rows and gathers them on
+               this rank, the single SRDB writer (srdb.py:116-126).
     """
 
     def __init__(self, precision: Optional[str] = None, commit: str = "fused",
-                 shard: Optional[tuple[int, int]] = None, device=None, graphs: Optional[bool] = None):
+                 shard: Optional[tuple[int, int]] = None, device=None, graphs: Optional[bool] = None,
+                 collect_root: int = 0):
         if commit not in ("fused", "checked"):
             raise ValueError("commit must be 'fused' or 'checked'")
         self._regions: dict[str, RegionDescriptor] = {}
@@ -204,6 +231,7 @@ class Runtime:
         self.commit = commit
         self.shard = shard
         self.graphs = graphs if graphs is not None else os.environ.get("SMLRT_GRAPHS", "1") != "0"
+        self.collect_root = collect_root
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
             else None)
@@ -341,8 +369,9 @@ class Runtime:
                                     self._staging.device_view(m.array, self.device)))
         return out
 
-    def _gather_dense(self, maps) -> Tensor:
-        """_combined_tensor (runtime.py:379-398) on the device."""
+    def _gather_dense(self, maps, rows=None) -> Tensor:
+        """_combined_tensor (runtime.py:379-398) on the device; `rows` = (r0, r1)
+        restricts it to a block of the flattened sweep ([r1 - r0, F])."""
         if not maps:
             raise MissingClauseError("region has no maps for this direction")
         groups, sweep = [], None
@@ -356,11 +385,14 @@ class Runtime:
             groups.append(views)
         dt = "f64" if any(m.array.dtype == "f64" for m in maps) else "f32"
         plan = build_plan(groups, "to")
-        out = torch.empty((plan.n_rows, plan.n_cols), device=self.device,
+        r0, r1 = rows if rows is not None else (0, plan.n_rows)
+        out = torch.empty((r1 - r0, plan.n_cols), device=self.device,
                           dtype=torch.float32 if dt == "f32" else torch.float64)
         ptrs, dts = plan.ptrs_and_dtypes()
-        _native.gather(plan.handle, ptrs, dts, out.data_ptr(), DTYPE_CODE[dt], 0, plan.n_rows,
+        _native.gather(plan.handle, ptrs, dts, out.data_ptr(), DTYPE_CODE[dt], r0, r1,
                        torch.cuda.current_stream(self.device).cuda_stream)
+        if rows is not None:
+            return Tensor(out)
         return Tensor(out.reshape(tuple(sweep) + (plan.n_cols,)))
 
     def _pinned(self, key, shape, dtype) -> torch.Tensor:
@@ -392,7 +424,74 @@ class Runtime:
             s = self._collect_side = torch.cuda.Stream(self.device)
         return s
 
+    def _collect_sharded(self) -> bool:
+        if self.shard is None or self.shard[1] <= 1:
+            return False
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized()
+
+    def _run_collect_sharded(self, desc, st) -> RegionOutcome:
+        """ml(collect) of a sharded region: each rank snapshots its block of
+        sweep rows, the blocks meet on the writer rank (gather_rows_to_root),
+        which appends the one record; every rank returns its index."""
+        import torch.distributed as dist
+        in_maps = self._device_maps(desc.in_maps + desc.inout_maps)
+        out_maps = self._device_maps(desc.out_maps + desc.inout_maps)
+        rank, world = self.shard
+        t0 = time.perf_counter_ns()
+        for m, d in zip(desc.in_maps + desc.inout_maps, in_maps):
+            self._staging.upload(m.array, d.array)
+        n_rows = self._plans_rows(in_maps)
+        rows = _shard_rows(n_rows, self.shard)
+        x_loc = self._gather_dense(in_maps, rows=rows).data
+        self._sync()
+        map_to = _ns_since(t0)
+        t0 = time.perf_counter_ns()
+        desc.accurate_fn()
+        self._sync()
+        region_ns = _ns_since(t0)
+        t0 = time.perf_counter_ns()
+        for m, d in zip(desc.out_maps + desc.inout_maps, out_maps):
+            self._staging.upload(m.array, d.array)
+        y_loc = self._gather_dense(out_maps, rows=rows).data
+        x_all = gather_rows_to_root(x_loc, n_rows, self.shard, root=self.collect_root)
+        y_all = gather_rows_to_root(y_loc, n_rows, self.shard, root=self.collect_root)
+        index = -1
+        if rank == self.collect_root:
+            xs = self._full_shape(in_maps, x_all)
+            ys = self._full_shape(out_maps, y_all)
+            x_host = self._pinned((desc.name, "in"), xs.shape, xs.dtype)
+            y_host = self._pinned((desc.name, "out"), ys.shape, ys.dtype)
+            x_host.copy_(xs)
+            y_host.copy_(ys)
+            index = self._db_for(desc).append_record(desc.name, x_host.numpy(), y_host.numpy(), region_ns)
+        idx = torch.tensor([index], dtype=torch.int64, device=self.device)
+        dist.broadcast(idx, src=self.collect_root)
+        map_from = _ns_since(t0)
+        st.accurate_calls += 1
+        st.accurate_ns += region_ns
+        st.map_to_ns += map_to
+        st.map_from_ns += map_from
+        st.records += 1
+        return RegionOutcome(path_taken=ACCURATE, elapsed_region_ns=region_ns,
+                             elapsed_map_to_ns=map_to, elapsed_map_from_ns=map_from,
+                             record_index=int(idx.item()))
+
+    @staticmethod
+    def _sweep_of(maps):
+        m = maps[0]
+        views = _views_for(m.functor, m.target, m.array)
+        return tuple(views[0].shape[: views[0].n_sweep])
+
+    def _plans_rows(self, maps) -> int:
+        return int(np.prod(self._sweep_of(maps), dtype=np.int64))
+
+    def _full_shape(self, maps, flat: torch.Tensor) -> torch.Tensor:
+        return flat.reshape(self._sweep_of(maps) + (flat.shape[-1],))
+
     def _run_collect(self, desc, st) -> RegionOutcome:
+        if self._collect_sharded():
+            return self._run_collect_sharded(desc, st)
         in_maps = self._device_maps(desc.in_maps + desc.inout_maps)
         out_maps = self._device_maps(desc.out_maps + desc.inout_maps)
         t0 = time.perf_counter_ns()

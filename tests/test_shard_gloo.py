@@ -71,3 +71,34 @@ def test_shard_rows_partition():
             assert blocks[0][0] == 0 and blocks[-1][1] == n
             for (a0, a1), (b0, b1) in zip(blocks, blocks[1:]):
                 assert a1 == b0 and a0 <= a1
+
+
+def _gather_worker(rank, world, port, n, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_18352_b200.runtime import gather_rows_to_root
+    full = torch.arange(n * 3, dtype=torch.float64).reshape(n, 3)
+    r0, r1 = _shard_rows(n, (rank, world))
+    got = gather_rows_to_root(full[r0:r1].clone(), n, (rank, world), root=world - 1)
+    if rank == world - 1:
+        out.put(got.numpy().tobytes())
+    else:
+        assert got is None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,world", [(7, 2), (1000, 3), (2, 3)])
+def test_collect_rows_meet_on_the_writer_rank(n, world):
+    """The collect snapshots of a sharded region (uneven last block, a rank
+    with no rows) reassemble in sweep order on the writer rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == np.arange(n * 3, dtype=np.float64).reshape(n, 3).tobytes()
