@@ -481,7 +481,6 @@ def e2e(wl, args, rank, world, dev, mdir, shard):
     import torch
     import paper_2407_18352_b200 as sm
     from paper_2407_18352_b200 import workloads
-    from paper_2407_18352_b200.runtime import _covers
     mw = wl.spec.name.startswith("miniweather")
     hw = workloads.make(wl.spec.name, wl.elements if not mw else None, seed_offset=0 if shard else rank)
     if mw and wl.elements != wl.spec.elements:
@@ -493,19 +492,16 @@ def e2e(wl, args, rank, world, dev, mdir, shard):
     torch.cuda.synchronize()
     barrier(world)
     e2e_steps = max(1, min(args.steps, 5))
+    b0 = (rt2._staging.h2d_bytes, rt2._staging.d2h_bytes)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         rt2.invoke_region(h2)
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev) / e2e_steps
-    _, _, ti, to = hw.functors()
-    h2d = hw.arrays[ti.array].nbytes
-    pout = rt2._plans[wl.spec.name + "_host"][2]
-    if shard is not None or not _covers(pout, rt2._staging.device_view(hw.buffers[to.array], dev)):
-        h2d += hw.arrays[to.array].nbytes
-    d2h = hw.arrays[to.array].nbytes + 4
-    if shard is not None:
-        h2d, d2h = h2d // world, d2h // world
+    # bytes the runtime actually moved per step (whole arrays, row ranges or
+    # window boxes), counted by its staging layer; + the 4-B status word
+    h2d = (rt2._staging.h2d_bytes - b0[0]) // e2e_steps
+    d2h = (rt2._staging.d2h_bytes - b0[1]) // e2e_steps + 4
     total = hw.elements if shard else world * hw.elements
     out = {"value": round(total / e2e_s, 1), "unit": "elements/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

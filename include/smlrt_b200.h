@@ -237,6 +237,18 @@ int smlrt_collect_async(const void* dense_dev, size_t bytes, void* pinned_host,
                         void* side_stream, void* after_event);
 int smlrt_collect_wait(void* side_stream);
 
+/*
+ * Host-path staging of a strided box (the e2e path of window functors, e.g.
+ * C4's [k, 0:128, 0:128] = ([k, 16:144, 16:144])): copies the elements
+ *   offset + z*slice + y*pitch + x,  x < width, y < height, z < depth
+ * of `src` to the same element positions of `dst` (one cudaMemcpy3DAsync:
+ * only the box's bytes cross PCIe).  direction: 0 host->device, 1
+ * device->host.  slice must be a multiple of pitch.
+ */
+int smlrt_copy_box_async(void* dst, const void* src, int64_t elem_size, int64_t offset, int64_t width,
+                         int64_t height, int64_t depth, int64_t pitch, int64_t slice, int32_t direction,
+                         void* stream);
+
 /* Diagnostic: one-CTA tcgen05 GEMM D[128 x N] = A[128 x K] * B[N x K]^T
  * (host f32 in, bf16 operands staged in the fused kernel's SW32/SW128
  * layouts, f32 out).  Validates descriptor encodings on a new device. */

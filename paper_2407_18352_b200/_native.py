@@ -100,6 +100,7 @@ SIGNATURES = {
     "smlrt_region_release": (_I, [_P]),
     "smlrt_collect_async": (_I, [_P, C.c_size_t, _P, _P, _P]),
     "smlrt_collect_wait": (_I, [_P]),
+    "smlrt_copy_box_async": (_I, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _P]),
     "smlrt_tc_selftest": (_I, [_I, _I, _P, _P, _P]),
     "smlrt_tc_selftest_ts": (_I, [_I, _I, _P, _P, _P]),
     "smlrt_fp32_peak": (_I, [_I32, C.POINTER(C.c_double)]),
@@ -345,6 +346,12 @@ def collect_async(dev_ptr, nbytes, host_ptr, side_stream, after_event):
 
 def collect_wait(side_stream):
     _check(lib().smlrt_collect_wait(side_stream))
+
+
+def copy_box_async(dst_ptr, src_ptr, elem_size, box, direction, stream):
+    """box = (offset, width, height, depth, pitch, slice) in elements."""
+    off, w, h, d, pitch, sl = box
+    _check(lib().smlrt_copy_box_async(dst_ptr, src_ptr, elem_size, off, w, h, d, pitch, sl, direction, stream))
 
 
 def tc_selftest(A, B, tmem_a: bool = False):

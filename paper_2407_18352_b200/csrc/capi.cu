@@ -564,6 +564,26 @@ extern "C" int smlrt_collect_async(const void* dense_dev, size_t bytes, void* pi
   return SMLRT_OK;
 }
 
+extern "C" int smlrt_copy_box_async(void* dst, const void* src, int64_t esz, int64_t offset, int64_t width,
+                                    int64_t height, int64_t depth, int64_t pitch, int64_t slice, int32_t direction,
+                                    void* stream) {
+  if (!dst || !src) return fail(SMLRT_E_INVALID, "copy_box: null pointer");
+  if (esz <= 0 || width <= 0 || height <= 0 || depth <= 0 || pitch < width || slice < pitch * height ||
+      slice % pitch != 0 || offset < 0)
+    return fail(SMLRT_E_INVALID, "copy_box: inconsistent box geometry");
+  const int64_t z0 = offset / slice, rem = offset % slice, y0 = rem / pitch, x0 = rem % pitch;
+  if (x0 + width > pitch) return fail(SMLRT_E_INVALID, "copy_box: box rows wrap the pitch");
+  cudaMemcpy3DParms p{};
+  p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), (size_t)(pitch * esz), (size_t)pitch, (size_t)(slice / pitch));
+  p.dstPtr = make_cudaPitchedPtr(dst, (size_t)(pitch * esz), (size_t)pitch, (size_t)(slice / pitch));
+  p.srcPos = make_cudaPos((size_t)(x0 * esz), (size_t)y0, (size_t)z0);
+  p.dstPos = p.srcPos;
+  p.extent = make_cudaExtent((size_t)(width * esz), (size_t)height, (size_t)depth);
+  p.kind = direction == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  SMLRT_CUDA(cudaMemcpy3DAsync(&p, (cudaStream_t)stream));
+  return SMLRT_OK;
+}
+
 extern "C" int smlrt_collect_wait(void* side_stream) {
   SMLRT_CUDA(cudaStreamSynchronize((cudaStream_t)side_stream));
   return SMLRT_OK;

@@ -175,6 +175,8 @@ class _Staging:
 
     def __init__(self):
         self._mirror: dict[int, tuple[torch.Tensor, ArrayBuffer]] = {}
+        self.h2d_bytes = 0  # host<->device bytes moved by the e2e path (instrumentation)
+        self.d2h_bytes = 0
 
     def device_view(self, a: ArrayBuffer, device: torch.device) -> ArrayBuffer:
         if a.is_device:
@@ -190,10 +192,12 @@ class _Staging:
     def upload(self, a: ArrayBuffer, dev_a: ArrayBuffer):
         if dev_a is not a:
             dev_a.data.copy_(a.data, non_blocking=a.data.is_pinned())
+            self.h2d_bytes += a.data.numel() * a.data.element_size()
 
     def download(self, a: ArrayBuffer, dev_a: ArrayBuffer):
         if dev_a is not a:
             a.data.copy_(dev_a.data, non_blocking=a.data.is_pinned())
+            self.d2h_bytes += a.data.numel() * a.data.element_size()
 
 
 class Runtime:
@@ -711,12 +715,21 @@ class Runtime:
             return None
         row_bytes = pin.n_cols * host_in[0].array.data.element_size()
         step = max(-(-self.STREAM_CHUNK_BYTES // row_bytes), -(-(r1 - r0) // self.STREAM_CHUNKS))
+        box = _window_box(pin)
         chunks = []
         for a in range(r0, r1, step):
             b = min(r1, a + step)
             ri = _native.plan_row_ranges(pin.handle, a, b)
             ro = _native.plan_row_ranges(pout.handle, a, b)
-            if ri is None or ro is None or not ro[1]:
+            if ro is None or not ro[1]:
+                return None
+            if box is not None and (ri is None or not ri[1]):
+                # a window functor: the chunk's windows as one strided box
+                # (exactly the window bytes, where merged ranges copy the gaps)
+                off, w, h, pitch, slice_ = box
+                chunks.append((a, b, ("box", (off + a * slice_, w, h, b - a, pitch, slice_)), ro[0]))
+                continue
+            if ri is None:
                 return None
             # gaps inside an input's ranges are copied too: allow at most 2x the touched elements
             if sum(hi - lo for lo, hi in ri[0]) > 2 * (b - a) * pin.n_cols:
@@ -740,8 +753,15 @@ class Runtime:
         down.wait_stream(cs)
         for a, b, in_ranges, out_ranges in chunks:
             with torch.cuda.stream(up):
-                for lo, hi in in_ranges:
-                    din[lo:hi].copy_(hin[lo:hi], non_blocking=True)
+                if in_ranges and in_ranges[0] == "box":
+                    bx = in_ranges[1]
+                    _native.copy_box_async(din.data_ptr(), hin.data_ptr(), hin.element_size(), bx, 0,
+                                           up.cuda_stream)
+                    self._staging.h2d_bytes += bx[1] * bx[2] * bx[3] * hin.element_size()
+                else:
+                    for lo, hi in in_ranges:
+                        din[lo:hi].copy_(hin[lo:hi], non_blocking=True)
+                        self._staging.h2d_bytes += (hi - lo) * hin.element_size()
             cs.wait_stream(up)
             _native.region_infer(pin.handle, iptr, idt, pout.handle, optr, odt, handle, a, b,
                                  _native.COMMIT_FUSED, None, cs.cuda_stream, status.data_ptr())
@@ -749,6 +769,7 @@ class Runtime:
             with torch.cuda.stream(down):
                 for lo, hi in out_ranges:
                     hout[lo:hi].copy_(dout[lo:hi], non_blocking=True)
+                    self._staging.d2h_bytes += (hi - lo) * hout.element_size()
         cs.wait_stream(down)
         bad = int(status.item())  # synchronises the stream
         infer_ns = _ns_since(t0)
@@ -770,6 +791,25 @@ class Runtime:
     def stats(self, handle: str) -> RegionStats:
         self._region(handle)
         return replace(self._stats[handle])
+
+
+def _window_box(plan: Plan):
+    """(offset, width, height, pitch, slice) of a window functor's in-plan --
+    one view, one sweep axis, a [height, width] window of rows `pitch`
+    elements apart, consecutive sweep rows `slice` elements apart (a multiple
+    of pitch) -- or None."""
+    if len(plan.views) != 1:
+        return None
+    _, v = plan.views[0]
+    if v.n_sweep != 1 or len(v.shape) != 3:
+        return None
+    slice_, pitch, one = v.strides
+    h, w = v.shape[1], v.shape[2]
+    if one != 1 or pitch < w or slice_ <= 0 or slice_ % pitch or slice_ < pitch * h:
+        return None
+    if v.base_offset % pitch + w > pitch:
+        return None
+    return v.base_offset, w, h, pitch, slice_
 
 
 def _same_sweeps(groups) -> bool:

@@ -279,6 +279,26 @@ def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, n, shard)
     assert np.array_equal(got, want)
 
 
+def test_chunked_host_path_window_box(cuda, tmp_path):
+    """A window functor's host input crosses PCIe as the windows only (one
+    strided 3-D copy per chunk), not whole frames; outputs bitwise the
+    device-resident call's."""
+    from paper_2407_18352_b200 import workloads
+    n = 300
+    dev_wl = workloads.make("particlefilter", n)
+    dev_wl.to_device()
+    host_wl = workloads.make("particlefilter", n)
+    host_wl.to_device(pinned_host=True)
+    sm.save_model(dev_wl.model, tmp_path / "m")
+    with _small_chunks(sm.Runtime()) as rt:
+        rt.invoke_region(rt.register_region(dev_wl.descriptor(str(tmp_path / "m"))))
+        h = rt.register_region(host_wl.descriptor(str(tmp_path / "m"), name="host"))
+        b0 = rt._staging.h2d_bytes
+        rt.invoke_region(h)
+        assert rt._staging.h2d_bytes - b0 == n * 128 * 128 * 4  # the windows, not the 160x160 frames
+    assert np.array_equal(host_wl.buffers["locs"].data.numpy(), dev_wl.buffers["locs"].data.cpu().numpy())
+
+
 def test_chunked_host_path_size_floor(cuda, tmp_path):
     """Below STREAM_MIN_BYTES the host buffers are staged whole (per-chunk
     host overhead would outweigh the overlap)."""
