@@ -1,15 +1,15 @@
-# build variant libraries of the stencil kernel (diagnostics): name and extra nvcc flags
+# build variant libraries (diagnostics): each variant recompiles ONE source
+# file with extra nvcc flags and links it with the main build's other objects.
+#   build_var <name> <file.cu> [flags...]  ->  paper_2407_18352_b200/libsmlrt_var_<name>.so
 set -e
 cd paper_2407_18352_b200/csrc
 build_var() {
-  name=$1; shift
+  name=$1; src=$2; shift 2
   mkdir -p build_var/$name
-  for f in plan kernels_simt exact_c1 exact_c5 exact_small exact_generic cnn_exact mlp_tc gemm_tc capi peak; do
-    cp -f build/$f.o build_var/$name/$f.o
-  done
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr "$@" -c stencil_tc.cu -o build_var/$name/stencil_tc.o
+  for o in build/*.o; do cp -f $o build_var/$name/; done
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v "$@" -c $src -o build_var/$name/${src%.cu}.o 2> build_var/$name/ptxas.txt || (cat build_var/$name/ptxas.txt; false)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libsmlrt_var_$name.so build_var/$name/*.o -lcudart
 }
-build_var rb32 -DSM_RB_=32
-build_var ns3 -DSM_NS_=3
-build_var ns4 -DSM_NS_=4
+build_var r2mb4 exact_c5.cu -DSMLRT_MW_R=2 -DSMLRT_EXACT_MINB=4
+build_var r2mb3 exact_c5.cu -DSMLRT_MW_R=2 -DSMLRT_EXACT_MINB=3
+build_var r1mb4 exact_c5.cu -DSMLRT_MW_R=1 -DSMLRT_EXACT_MINB=4
