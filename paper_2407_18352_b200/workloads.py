@@ -199,6 +199,6 @@ def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Worklo
 
 
 def _grid_for(elements: int):
-    nz = 2048 if elements >= 4096 * 64 else 130
+    nz = 2048 if elements >= 4096 * 64 else 132  # a 16-B multiple row pitch (TMA-able)
     nx = max(3, elements // (nz - 2) + 2)
     return nx, nz

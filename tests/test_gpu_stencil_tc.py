@@ -104,36 +104,34 @@ def test_stencil_tc_full_size(cuda, tmp_path):
     _check(wl, got)
 
 
-def test_stencil_tc_nonfinite(cuda, tmp_path):
-    wl = workloads.make("miniweather_bf16", 38 * 128)  # 40 x 130 grid -> not TMA-aligned: the layer chain
-    assert wl.arrays["state"].shape[2] % 4 != 0
-    wl.arrays["state"][2, 10, 20] = np.inf
+def _mw(nx, nz):
+    wl = workloads.make("miniweather_bf16", (nx - 2) * (nz - 2))
+    st = np.stack([workloads._bumps(nx, nz, k) for k in range(4)]).astype(np.float32)
+    wl.arrays = {"state": st, "state_new": np.zeros_like(st)}
+    wl.env = {"NX": nx, "NZ": nz}
+    return wl
+
+
+@pytest.mark.parametrize("nz,launches", [(132, 2), (130, 4)])  # stencil kernel / layer chain, + the gated scatter
+@pytest.mark.parametrize("bad", [np.inf, np.nan])
+def test_stencil_nonfinite(cuda, tmp_path, nz, launches, bad):
+    wl = _mw(40, nz)
+    wl.arrays["state"][2, 10, 20] = bad
     wl.to_device()
     sm.save_model(wl.model, tmp_path / "mw")
+    n0 = _native.launch_count()
     with sm.Runtime(commit="checked") as rt:
         with pytest.raises(NonFiniteOutputError):
             rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "mw"))))
+    assert _native.launch_count() - n0 == launches
     assert (wl.buffers["state_new"].to_numpy() == 0).all()
 
 
 def test_stencil_unaligned_pitch_uses_chain(cuda, tmp_path):
     """A row pitch that is not a multiple of 4 elements cannot be a TMA
     stride: the region runs on the generic layer chain, same tolerance."""
-    nx, nz = 20, 130
-    wl = workloads.make("miniweather_bf16", (nx - 2) * (nz - 2))
-    assert wl.arrays["state"].shape == (4, nx, nz)
+    wl = _mw(20, 130)
     n0 = _native.launch_count()
     got = _run(wl, tmp_path)
     assert _native.launch_count() - n0 == 4  # gather, two GEMMs, scatter
     _check(wl, got, emulate=False)  # the chain quantises to bf16 throughout
-
-
-def test_stencil_nonfinite_tc(cuda, tmp_path):
-    wl = workloads.make("miniweather_bf16", 38 * 130)
-    wl.arrays["state"][1, 10, 20] = np.nan
-    wl.to_device()
-    sm.save_model(wl.model, tmp_path / "mw")
-    with sm.Runtime(commit="checked") as rt:
-        with pytest.raises(NonFiniteOutputError):
-            rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "mw"))))
-    assert (wl.buffers["state_new"].to_numpy() == 0).all()
