@@ -176,8 +176,11 @@ __device__ __forceinline__ void mma_1688_tf32(float (&d)[4], const uint32_t (&a)
         "f"(c[3]));
 }
 
+#ifndef SM_MINB
+#define SM_MINB 4
+#endif
 template <int NT1, int ACT1, bool G4>
-__global__ void __launch_bounds__(128, 4) stencil_mma_kernel(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(128, SM_MINB) stencil_mma_kernel(const __grid_constant__ CUtensorMap tm,
                                                              const __grid_constant__ SmArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // (indexing the __shared__ array keeps the loads in the shared window: LDS, ordered after the waits)
