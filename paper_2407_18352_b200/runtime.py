@@ -715,6 +715,8 @@ class Runtime:
             return None
         row_bytes = pin.n_cols * host_in[0].array.data.element_size()
         step = max(-(-self.STREAM_CHUNK_BYTES // row_bytes), -(-(r1 - r0) // self.STREAM_CHUNKS))
+        if len(pin.sweep) == 2:
+            return self._band_chunks(pin, pout, r0, r1, step)
         box = _window_box(pin)
         chunks = []
         for a in range(r0, r1, step):
@@ -735,6 +737,26 @@ class Runtime:
             if sum(hi - lo for lo, hi in ri[0]) > 2 * (b - a) * pin.n_cols:
                 return None
             chunks.append((a, b, ri[0], ro[0]))
+        return chunks
+
+    def _band_chunks(self, pin, pout, r0, r1, step):
+        """2-D sweeps (a halo stencil over grid rows): chunks are bands of whole
+        sweep rows; each band's input (its rows plus the halo) and output (the
+        band's interior) are strided 3-D boxes, copied exactly."""
+        bi, bo = _sweep_box(pin), _sweep_box(pout)
+        if bi is None or bo is None or tuple(pout.sweep) != tuple(pin.sweep):
+            return None
+        nj = pin.sweep[1]
+        if r0 % nj or (r1 % nj and r1 != pin.n_rows):
+            return None
+        rows_per = max(1, step // nj)
+        chunks = []
+        for ia in range(r0 // nj, -(-r1 // nj), rows_per):
+            ib = min(-(-r1 // nj), ia + rows_per)
+            boxes = []
+            for (off, w, h, d, pitch, slice_, s0) in (bi, bo):
+                boxes.append(("box", (off + ia * s0, w, h + (ib - ia) - 1, d, pitch, slice_)))
+            chunks.append((ia * nj, min(r1, ib * nj), boxes[0], [boxes[1]]))
         return chunks
 
     def _run_streamed(self, st, hin_map, din_map, hout_map, dout_map, pin, pout, chunks, handle, map_to):
@@ -767,7 +789,14 @@ class Runtime:
                                  _native.COMMIT_FUSED, None, cs.cuda_stream, status.data_ptr())
             down.wait_stream(cs)
             with torch.cuda.stream(down):
-                for lo, hi in out_ranges:
+                for rng in out_ranges:
+                    if rng[0] == "box":
+                        bx = rng[1]
+                        _native.copy_box_async(hout.data_ptr(), dout.data_ptr(), hout.element_size(), bx, 1,
+                                               down.cuda_stream)
+                        self._staging.d2h_bytes += bx[1] * bx[2] * bx[3] * hout.element_size()
+                        continue
+                    lo, hi = rng
                     hout[lo:hi].copy_(dout[lo:hi], non_blocking=True)
                     self._staging.d2h_bytes += (hi - lo) * hout.element_size()
         cs.wait_stream(down)
@@ -810,6 +839,41 @@ def _window_box(plan: Plan):
     if v.base_offset % pitch + w > pitch:
         return None
     return v.base_offset, w, h, pitch, slice_
+
+
+def _sweep_box(plan: Plan):
+    """The elements a 2-D sweep plan touches as a 3-D box per sweep row, or
+    None: sweep strides (s0, 1) and either one view whose feature axes are
+    (planes, rows, columns) with strides (slice, s0, 1) -- the halo in-functor
+    -- or point views whose bases step by a constant multiple of s0 -- one per
+    output plane.  Returns (offset of sweep row 0, width, height of one sweep
+    row, depth, pitch, slice, s0): band [ia, ib) spans height + ib - ia - 1
+    rows from offset + ia*s0."""
+    views = [v for _, v in plan.views]
+    if not views or any(v.n_sweep != 2 for v in views):
+        return None
+    s0 = views[0].strides[0]
+    if any(v.strides[:2] != (s0, 1) for v in views) or s0 <= 0:
+        return None
+    nj = views[0].shape[1]
+    if len(views) == 1 and len(views[0].shape) == 5:
+        v = views[0]
+        d, h, w = v.shape[2:]
+        slice_, pitch, one = v.strides[2:]
+        if pitch != s0 or one != 1 or slice_ % s0 or slice_ < s0 * h:
+            return None
+        off, width, height, depth = v.base_offset, nj + w - 1, h, d
+    elif all(int(np.prod(v.shape[2:])) == 1 for v in views):
+        bases = [v.base_offset for v in views]
+        slice_ = bases[1] - bases[0] if len(bases) > 1 else s0 * (1 << 20)
+        if any(b1 - b0 != slice_ for b0, b1 in zip(bases, bases[1:])) or slice_ <= 0 or slice_ % s0:
+            return None
+        off, width, height, depth = bases[0], nj, 1, len(bases)
+    else:
+        return None
+    if off % s0 + width > s0:
+        return None
+    return off, width, height, depth, s0, slice_, s0
 
 
 def _same_sweeps(groups) -> bool:

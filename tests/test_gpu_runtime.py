@@ -254,7 +254,9 @@ def _small_chunks(rt):
 
 @pytest.mark.parametrize("config,n,shard", [("bonds", 312345, None), ("bonds", 312345, (1, 3)),
                                             ("options", 312345, None), ("minibude", 312345, None),
-                                            ("minibude", 312345, (0, 2)), ("particlefilter", 601, None)])
+                                            ("minibude", 312345, (0, 2)), ("particlefilter", 601, None),
+                                            ("miniweather", 130 * 300, None), ("miniweather_bf16", 130 * 300, None),
+                                            ("miniweather", 130 * 300, (1, 3))])
 def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, n, shard):
     """Pinned host input/output over uniform 1-D plans (AoS rows, SoA columns,
     2-D windows) take the chunked three-stream path (H2D / kernel / D2H
@@ -277,6 +279,27 @@ def test_chunked_host_path_matches_device_path(cuda, tmp_path, config, n, shard)
     got = host_wl.buffers[to.array].data.numpy()
     want = dev_wl.buffers[to.array].data.cpu().numpy()
     assert np.array_equal(got, want)
+
+
+def test_chunked_host_path_grid_bands(cuda, tmp_path):
+    """A 2-D sweep (the halo stencil) streams in bands of grid rows: each
+    band's input rows + halo and its output interior cross PCIe as strided
+    boxes -- the border of the host output is never written."""
+    from paper_2407_18352_b200 import workloads
+    wl = workloads.make("miniweather", 130 * 300)
+    wl.arrays["state_new"][:] = 7.0
+    wl.to_device(pinned_host=True)
+    sm.save_model(wl.model, tmp_path / "m")
+    with _small_chunks(sm.Runtime()) as rt:
+        h = rt.register_region(wl.descriptor(str(tmp_path / "m")))
+        b0 = rt._staging.h2d_bytes, rt._staging.d2h_bytes
+        rt.invoke_region(h)
+        nx, nz = wl.arrays["state"].shape[1:]
+        assert rt._staging.d2h_bytes - b0[1] == 4 * (nx - 2) * (nz - 2) * 4  # interiors only
+        assert rt._staging.h2d_bytes - b0[0] < 1.2 * wl.arrays["state"].nbytes  # bands + 2 halo rows each
+    out = wl.buffers["state_new"].data.numpy().reshape(wl.arrays["state"].shape)
+    assert (out[:, 0, :] == 7.0).all() and (out[:, -1, :] == 7.0).all()
+    assert (out[:, :, 0] == 7.0).all() and (out[:, :, -1] == 7.0).all()
 
 
 def test_chunked_host_path_window_box(cuda, tmp_path):
