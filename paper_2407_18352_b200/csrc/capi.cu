@@ -68,6 +68,7 @@ smlrt_model_s::~smlrt_model_s() {
   }
   cudaFree(tc_blob);
   cudaFree(chain_blob);
+  cudaFree(smm_blob);
   cudaSetDevice(prev);
 }
 

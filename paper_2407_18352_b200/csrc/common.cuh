@@ -191,6 +191,8 @@ struct smlrt_model_s {
   std::vector<ChainLayer> chain;
   void* chain_blob = nullptr;
   int chain_first = -1;  // model layer the chain starts at (CNN: the first dense layer)
+  // small-MLP warp-MMA kernel (small_mma.cu): per-lane B fragments + biases
+  void* smm_blob = nullptr;
   ~smlrt_model_s();
 };
 
@@ -235,6 +237,10 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
                        const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out, int64_t r0,
                        int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 // bf16 halo-stencil regions on tcgen05 (stencil_tc.cu); SMLRT_E_UNSUPPORTED if not that shape
+int small_mma_pack(smlrt_model_s& m);
+int launch_region_small_mma(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
+                            const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
+                            int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 int launch_region_stencil_tc(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
                              const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
                              int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);

@@ -1127,6 +1127,7 @@ __global__ void __launch_bounds__(128, 1) tc_selftest_kernel(const float* A, con
 
 int tc_pack_model(smlrt_model_s& m) {
   if (int rc = chain_pack(m)) return rc;  // the generic fallback of every dense model
+  if (int rc = small_mma_pack(m)) return rc;  // small 3-layer MLPs (warp-MMA kernel)
   if (wide_shape(m)) return wide_pack(m);
   // [single-CTA blob][pad to 1 KB][rank-0 blob][rank-1 blob]
   std::vector<uint8_t> blob, pair;
@@ -1139,6 +1140,7 @@ int tc_pack_model(smlrt_model_s& m) {
     blob = pack<128, 64, 1>(m);
     pair = pack<128, 64, 2>(m);
     off = pair_blob_off<128, 64>();
+
   } else {
     return SMLRT_OK;  // no tcgen05 kernel for this shape; region_infer reports it
   }
@@ -1161,6 +1163,11 @@ int launch_region_tc(const smlrt_model_s& m, const DevPlan& in, const void* cons
                : SMLRT_E_UNSUPPORTED;
   // halo stencils over a 2-D sweep (C5 shape): the plan decides, not the model alone
   int rc = launch_region_stencil_tc(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, r0, r1, staged, s, status);
+  if (rc != SMLRT_E_UNSUPPORTED) return rc;
+  // small 3-layer MLPs (C1's 5-64-32-1 at bf16): one warp-MMA kernel with the
+  // activations in registers (the bonds-family tcgen05 kernel instantiated at
+  // 64-32 measured 63 us on C1 vs 36.5 us: its per-tile handshakes dominate)
+  rc = launch_region_small_mma(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, r0, r1, staged, s, status);
   if (rc != SMLRT_E_UNSUPPORTED) return rc;
   if (m.tc_blob != nullptr) {
     if (wide_shape(m))

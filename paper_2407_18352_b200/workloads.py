@@ -55,6 +55,10 @@ CONFIGS = {
     "options": Spec("options", 1_000_000, [5, 64, 32, 1], "fp32",
                     "functor(optin: [k, 0:5] = ([k, 0:5]))", "functor(optout: [k, 0:1] = ([k]))",
                     "map(to: optin(recs[0:N]))", "map(from: optout(price[0:N]))", "fp32", 24),
+    # the same region at bf16: all three layers on warp-level tensor-core MMAs
+    "options_bf16": Spec("options_bf16", 1_000_000, [5, 64, 32, 1], "bf16",
+                         "functor(optin: [k, 0:5] = ([k, 0:5]))", "functor(optout: [k, 0:1] = ([k]))",
+                         "map(to: optin(recs[0:N]))", "map(from: optout(price[0:N]))", "hbm", 24),
     "bonds": Spec("bonds", 16_777_216, [16, 256, 128, 1], "bf16",
                   "functor(bin: [k, 0:16] = ([k, 0:16]))", "functor(bout: [k, 0:1] = ([k]))",
                   "map(to: bin(bonds[0:N]))", "map(from: bout(val[0:N]))", "tensor", 68),
@@ -167,7 +171,7 @@ def make(name: str, elements: int | None = None, seed_offset: int = 0) -> Worklo
         layers = init_weights(s.dims)
         model = Model(s.dims[0], s.dims[-1], [DenseLayer(w, b, a) for w, b, a in layers],
                       precision=s.precision)
-    if name == "options":
+    if name.startswith("options"):
         n = elements or s.elements
         rng = np.random.default_rng(0 + seed_offset)
         recs = np.stack([rng.uniform(lo, hi, n) for lo, hi in _OPT_RANGES], 1).astype(np.float32)
