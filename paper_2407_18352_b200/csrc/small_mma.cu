@@ -98,13 +98,20 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  uint32_t w1[T1][2], w2[T2][K2][2], w3[K3][2];
+  uint32_t w1[T1][2], w3[K3][2];
 #pragma unroll
   for (int t = 0; t < T1; ++t) w1[t][0] = sf.w1[t][lane][0], w1[t][1] = sf.w1[t][lane][1];
+#ifndef SMM_W2_SMEM
+  uint32_t w2[T2][K2][2];
 #pragma unroll
   for (int t = 0; t < T2; ++t)
 #pragma unroll
     for (int k = 0; k < K2; ++k) w2[t][k][0] = sf.w2[t][k][lane][0], w2[t][k][1] = sf.w2[t][k][lane][1];
+#define SMM_W2(t, k, i) w2[t][k][i]
+#else
+  // layer-2 fragments read from shared memory per use (fewer registers, more warps)
+#define SMM_W2(t, k, i) sf.w2[t][k][lane][i]
+#endif
 #pragma unroll
   for (int k = 0; k < K3; ++k) w3[k][0] = sf.w3[k][lane][0], w3[k][1] = sf.w3[k][lane][1];
   // A of the bias steps: (1, 0) at k = 0 of the step for quad member 0
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
 #pragma unroll
     for (int t = 0; t < T2; ++t) {
       d2[t][0] = d2[t][1] = d2[t][2] = d2[t][3] = 0.0f;
-      mma_bf16(d2[t], abias, w2[t][K2 - 1][0], w2[t][K2 - 1][1]);
+      mma_bf16(d2[t], abias, SMM_W2(t, K2 - 1, 0), SMM_W2(t, K2 - 1, 1));
     }
 #pragma unroll
     for (int k = 0; k < K2 - 1; ++k) {
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
                               act_pack<ACT1>(d1[2 * k + 1][0], d1[2 * k + 1][1]),
                               act_pack<ACT1>(d1[2 * k + 1][2], d1[2 * k + 1][3])};
 #pragma unroll
-      for (int t = 0; t < T2; ++t) mma_bf16(d2[t], af, w2[t][k][0], w2[t][k][1]);
+      for (int t = 0; t < T2; ++t) mma_bf16(d2[t], af, SMM_W2(t, k, 0), SMM_W2(t, k, 1));
     }
     // layer 3 (bf16, N = 8 holds the outputs)
     float y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -198,6 +205,7 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
   }
   if (__any_sync(0xffffffffu, chk != chk) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
 }
+#undef SMM_W2
 
 uint32_t smm_bits(float f) {
   uint32_t u;

@@ -139,3 +139,15 @@ def test_mixed_activations_use_the_chain(cuda, tmp_path):
     assert launches == 5  # the layer chain: gather, three GEMMs, scatter
     ref, _ = c_oracle.mlp_f32(wl.layers, wl.arrays["recs"])
     assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()
+
+
+def test_f64_arrays_take_the_chain(cuda, tmp_path):
+    """f64 application arrays (computed in f32, stored back as f64,
+    models.py:211-223) fall back from the f32-only warp-MMA kernel to the
+    layer chain, same tolerance."""
+    wl = _region([5, 64, 32, 1], 2049, "relu")
+    wl.arrays = {k: v.astype(np.float64) for k, v in wl.arrays.items()}
+    got, launches = _run(wl, tmp_path)
+    assert launches == 5 and got.dtype == np.float64
+    ref, _ = c_oracle.mlp_f32(wl.layers, wl.arrays["recs"].astype(np.float32))
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()

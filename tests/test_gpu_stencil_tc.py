@@ -135,3 +135,12 @@ def test_stencil_unaligned_pitch_uses_chain(cuda, tmp_path):
     got = _run(wl, tmp_path)
     assert _native.launch_count() - n0 == 4  # gather, two GEMMs, scatter
     _check(wl, got, emulate=False)  # the chain quantises to bf16 throughout
+
+
+def test_stencil_f64_takes_the_chain(cuda, tmp_path):
+    wl = _mw(20, 132)
+    wl.arrays = {k: v.astype(np.float64) for k, v in wl.arrays.items()}
+    n0 = _native.launch_count()
+    got = _run(wl, tmp_path)
+    assert _native.launch_count() - n0 == 4 and got.dtype == np.float64
+    _check(wl, got.astype(np.float32), emulate=False)

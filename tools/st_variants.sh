@@ -10,6 +10,4 @@ build_var() {
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v "$@" -c $src -o build_var/$name/${src%.cu}.o 2> build_var/$name/ptxas.txt || (cat build_var/$name/ptxas.txt; false)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libsmlrt_var_$name.so build_var/$name/*.o -lcudart
 }
-build_var lb6 stencil_tc.cu -DSM_MINB=6
-build_var lb7 stencil_tc.cu -DSM_MINB=7
-build_var lb6br8 stencil_tc.cu -DSM_MINB=6 -DSM_BR_=8
+build_var w2s small_mma.cu -DSMM_W2_SMEM
