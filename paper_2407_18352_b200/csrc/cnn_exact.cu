@@ -27,8 +27,7 @@
 
 namespace smlrt {
 
-int make_map_f32_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                    uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, int promote);
+
 
 namespace {
 
@@ -246,6 +245,20 @@ __device__ __forceinline__ uint64_t cadd2(uint64_t acc, uint64_t p, uint64_t one
   return r;
 }
 
+// Window loads with a 64-B L2 prefetch-size hint.  A 512-B window row starts
+// 64 B into a 128-B line; with the default fetch size the L2 reads whole
+// 128-B lines from DRAM (1.342 GB for 1.074 GB of windows on C4, measured, the
+// same through TMA with or without L2 promotion); `.L2::64B` fetches only the
+// touched 64-B halves: DRAM reads = the window bytes (1.08 GB), C4's conv
+// front 195 -> 158 us.
+__device__ __forceinline__ float4 ld_window(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::64B.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_constant__ FrontArgs a,
                                                               const __grid_constant__ DevPlan P,
                                                               const __grid_constant__ ConvW8 cw) {
@@ -265,8 +278,8 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
   float4 u[8][2];
 #pragma unroll
   for (int dy = 0; dy < 8; ++dy) {  // all 16 loads in flight before the math
-    u[dy][0] = __ldg(reinterpret_cast<const float4*>(prow + dy * pitch));
-    u[dy][1] = __ldg(reinterpret_cast<const float4*>(prow + dy * pitch) + 1);
+    u[dy][0] = ld_window(reinterpret_cast<const float4*>(prow + dy * pitch));
+    u[dy][1] = ld_window(reinterpret_cast<const float4*>(prow + dy * pitch) + 1);
   }
   uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
@@ -292,83 +305,6 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
   const int64_t orr = row - a.r0;
   if (a.pool == 2) {
     // 2x2 window = lanes {l, l^1, l^16, l^17}; NaN propagates like np.max
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      float m = max_nan(y[o], __shfl_xor_sync(0xffffffffu, y[o], 1));
-      m = max_nan(m, __shfl_xor_sync(0xffffffffu, m, 16));
-      y[o] = m;
-    }
-    if (lane < 16 && (lane & 1) == 0) {
-#pragma unroll
-      for (int o = 0; o < 8; ++o) put_feat(a, orr, o * 64 + warp * 8 + (lane >> 1), y[o]);
-    }
-  } else {
-#pragma unroll
-    for (int o = 0; o < 8; ++o) put_feat(a, orr, o * 256 + py * 16 + px, y[o]);
-  }
-}
-
-// The same C4 front with the 128 x 128 window brought in by ONE TMA load per
-// frame (3-D tensor map over [frames][rows][pitch], box 1 x 128 x 128 at the
-// window origin, no L2 sector promotion) instead of 16 LDG.128 per thread:
-// the LDG path fetched whole 128-B lines around each 512-B window row (640 B
-// of a 640-B frame row: 1.25x the window bytes from DRAM).  Each thread then
-// reads its 8 x 8 patch from shared memory, the two 16-B halves of a patch
-// row in lane-dependent order so the 8 lanes of a quarter-warp hit distinct
-// bank groups.
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(ptx::smem_u32(bar))
-      : "memory");
-}
-
-__global__ void __launch_bounds__(256) conv_pool_tma_kernel(const __grid_constant__ CUtensorMap tm,
-                                                            const __grid_constant__ FrontArgs a, int x0, int y0,
-                                                            int64_t z0, const __grid_constant__ ConvW8 cw) {
-  extern __shared__ __align__(128) float win[];  // [128][128]
-  __shared__ uint64_t bar;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int py = 2 * warp + (lane >> 4), px = lane & 15;
-  const int64_t row = a.r0 + blockIdx.x;
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(&bar, 1);
-    ptx::mbar_fence_init();
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ptx::smem_u32(&bar)), "r"(128 * 128 * 4)
-                 : "memory");
-    tma_load_3d(ptx::smem_u32(win), &tm, &bar, x0, y0, (int)(z0 + row));
-  }
-  __syncthreads();
-  ptx::mbar_wait(&bar, 0);
-  const float* prow = win + (py * 8) * 128 + px * 8;
-  const int h = (px >> 2) & 1;  // which 16-B half first: distinct banks per quarter-warp
-  uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-  for (int dy = 0; dy < 8; ++dy) {
-    const float4 f0 = *reinterpret_cast<const float4*>(prow + dy * 128 + 4 * h);
-    const float4 f1 = *reinterpret_cast<const float4*>(prow + dy * 128 + 4 * (h ^ 1));
-    const float4 lo = h ? f1 : f0, hi = h ? f0 : f1;
-    const float v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-    for (int dx = 0; dx < 8; ++dx) {
-      const uint64_t vv = cpk2(v[dx], v[dx]);
-      const float* wf = cw.w + (dy * 8 + dx) * 8;
-#pragma unroll
-      for (int op = 0; op < 4; ++op)
-        acc[op] = cadd2(acc[op], cmul2(vv, *reinterpret_cast<const uint64_t*>(wf + 2 * op)), cw.one2);
-    }
-  }
-  float y[8];
-#pragma unroll
-  for (int op = 0; op < 4; ++op) {
-    cupk2(cadd2(acc[op], *reinterpret_cast<const uint64_t*>(cw.b + 2 * op), cw.one2), y[2 * op], y[2 * op + 1]);
-    y[2 * op] = act_exact(y[2 * op], a.act);
-    y[2 * op + 1] = act_exact(y[2 * op + 1], a.act);
-  }
-  const int64_t orr = row - a.r0;
-  if (a.pool == 2) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
       float m = max_nan(y[o], __shfl_xor_sync(0xffffffffu, y[o], 1));
@@ -520,7 +456,7 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
 
 int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const void* src, int src_dt,
                  int64_t r0, int64_t r1, float* out, int* out_w, int* next_layer, cudaStream_t s,
-                 int64_t src_array_elems = 0, __nv_bfloat16* out_bf = nullptr, int out_pitch = 0) {
+                 __nv_bfloat16* out_bf = nullptr, int out_pitch = 0) {
   const DevLayer& c = m.layers[0];
   FrontArgs a{};
   a.x = x;
@@ -571,41 +507,8 @@ int launch_front(const smlrt_model_s& m, const float* x, const DevPlan* P, const
     for (int o = 0; o < 8; ++o) cw.b[o] = hw[64 * 8 + o];
     const float one[2] = {1.0f, 1.0f};
     std::memcpy(&cw.one2, one, sizeof(one));
-    // SMLRT_PF_TMA=1 (no L2 promotion) / 2 (128-B promotion): the window by
-    // one TMA load per frame.  Measured on C4: DRAM reads 1.342 GB in all
-    // three modes (L2 sees 640 B per 512-B window row either way: the rows
-    // start 64 B into a 128-B line), kernel time equal (0.324 ms region) --
-    // the over-fetch is the window's line alignment, not the load path.
-    // Default: the LDG kernel (no shared memory, higher occupancy).
-    static const int tma_mode = [] {
-      const char* e = std::getenv("SMLRT_PF_TMA");
-      return e ? std::atoi(e) : 0;
-    }();
-    bool launched = false;
-    if (tma_mode && P != nullptr && a.x == nullptr && P->n_sweep == 1 && P->win_pitch > 0 &&
-        P->ustride[0] % P->win_pitch == 0 && src_array_elems > 0) {
-      const int64_t pitch = P->win_pitch, fs = P->ustride[0];
-      const int64_t z0 = P->col_off0 / fs, rem = P->col_off0 % fs;
-      const int x0 = (int)(rem % pitch), y0 = (int)(rem / pitch);
-      const int64_t nz = src_array_elems / fs;
-      CUtensorMap tm;
-      if (x0 + 128 <= pitch && y0 + 128 <= fs / pitch && nz >= z0 + r1 &&
-          make_map_f32_3d(&tm, src, (uint64_t)pitch, (uint64_t)(fs / pitch), (uint64_t)nz, (uint64_t)pitch * 4,
-                          (uint64_t)fs * 4, 128, 128, 1, tma_mode == 2 ? 128 : 0) == SMLRT_OK) {
-        static int cfg = 0;
-        if (!cfg) {
-          SMLRT_CUDA(cudaFuncSetAttribute(conv_pool_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-          cfg = 1;
-        }
-        conv_pool_tma_kernel<<<(unsigned)(r1 - r0), 256, 65536, s>>>(tm, a, x0, y0, z0, cw);
-        count_launch();
-        launched = true;
-      }
-    }
-    if (!launched) {
-      conv_pool_k8oc8_kernel<<<(unsigned)(r1 - r0), 256, 0, s>>>(a, P ? *P : dummy, cw);
-      count_launch();
-    }
+    conv_pool_k8oc8_kernel<<<(unsigned)(r1 - r0), 256, 0, s>>>(a, P ? *P : dummy, cw);
+    count_launch();
   } else if (a.C == 1 && a.K == 8 && a.OC == 8 && aligned) {
     conv_front_fixed_kernel<8, 8><<<(unsigned)(r1 - r0), 256, smem, s>>>(a, P ? *P : dummy);
     count_launch();
@@ -736,8 +639,8 @@ int launch_region_cnn_bf16(const smlrt_model_s& m, const DevPlan& in, const void
     // the chain's ping-pong reuses act0 at another pitch
     if (m.layers[m.chain_first - 1].out < k0) SMLRT_CUDA(cudaMemsetAsync(act0, 0, (size_t)n * k0 * 2, s));
     int ow = 0, nl = 0;
-    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, nullptr, &ow, &nl, s,
-                      in.uarray_numel, act0, k0);
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, nullptr, &ow, &nl, s, act0,
+                      k0);
     if (rc) break;
     if (nl != m.chain_first) {
       rc = fail(SMLRT_E_UNSUPPORTED, "bf16 CNN: front and chain disagree on the first dense layer");
@@ -809,8 +712,7 @@ int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* con
     float* t1 = t0 + per * ch;
     float* yo = t1 + per * ch;
     int ow, nl;
-    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, sa,
-                      in.uarray_numel);
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, sa);
     if (rc) break;
     if (sa != sb) {
       cudaEvent_t e = event();

@@ -10,4 +10,4 @@ build_var() {
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v "$@" -c $src -o build_var/$name/${src%.cu}.o 2> build_var/$name/ptxas.txt || (cat build_var/$name/ptxas.txt; false)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libsmlrt_var_$name.so build_var/$name/*.o -lcudart
 }
-build_var w2s small_mma.cu -DSMM_W2_SMEM
+build_var l264 cnn_exact.cu -DSMLRT_PF_L2_64B
