@@ -49,6 +49,7 @@ from .bridge import (
 )
 from .directives import FunctorDecl, MapTarget, MlDirective
 from .errors import (
+    DeviceError,
     DuplicateRegionError,
     InvalidScheduleError,
     MissingClauseError,
@@ -628,9 +629,12 @@ class Runtime:
             # and settings replay a prepared native call (a CUDA graph of
             # this call's launches) with these arguments
             if all(m.array.is_device for m in host_in):
-                self._fast[desc.name] = (self._fast_key(desc, model), _native.prepare_region(
-                    pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1, flags, status.data_ptr(),
-                    pin, pout, model, graph=self.graphs))
+                try:
+                    self._fast[desc.name] = (self._fast_key(desc, model), _native.prepare_region(
+                        pin.handle, iptr, idt, pout.handle, optr, odt, handle, r0, r1, flags, status.data_ptr(),
+                        pin, pout, model, graph=self.graphs))
+                except DeviceError:
+                    self._fast.pop(desc.name, None)  # no prepared call: every call takes this path
         else:
             status.zero_()
         if self.time_kernels:
