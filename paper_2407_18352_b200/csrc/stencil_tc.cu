@@ -39,6 +39,7 @@
 #include "common.cuh"
 #include "simt_common.cuh"
 #include "tc_ptx.cuh"
+#include "stencil_common.cuh"
 
 namespace smlrt {
 
@@ -48,6 +49,7 @@ int make_map_f32_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1
 namespace {
 
 using namespace ptx;
+using namespace stencil;
 
 #ifndef SM_BR_
 #define SM_BR_ 4
@@ -99,33 +101,6 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4],
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]), "f"(c[2]),
         "f"(c[3]));
-}
-
-// one box of the 3-D tensor map (columns, rows of a plane, planes)
-__device__ __forceinline__ void sm_tma(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void sm_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// mbarrier wait that traps after ~2^26 polls (seconds): a TMA that never
-// lands fails the launch instead of hanging the device
-__device__ __forceinline__ void sm_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  for (uint32_t n = 0;; ++n) {
-    uint32_t ok;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (n > (1u << 26)) __trap();
-  }
 }
 
 __device__ __forceinline__ float sm_act(float y, int act) {
@@ -362,35 +337,6 @@ uint32_t sm_bf16(float f) {
 }
 uint32_t sm_pair(float lo, float hi) { return sm_bf16(lo) | (sm_bf16(hi) << 16); }
 
-// The in-plan is the 4-variable 3x3 halo functor over a 2-D sweep with unit
-// inner stride -- run (v, d) starts at col_inl[(v*3 + d)*3] = first_v + d*s0,
-// the variables' planes equally spaced by a multiple of s0 -- and every
-// element read lies inside the s0-pitched rows (no wrap).  Fills the box
-// origin; false if the plan has another shape.
-bool stencil_shape(const DevPlan& in, SmArgs& a, int64_t* plane) {
-  if (!in.uniform || in.n_sweep != 2 || in.ustride[1] != 1 || in.n_cols != 36) return false;
-  const int64_t s0 = in.ustride[0], nj = in.sdiv[1].d, numel = in.uarray_numel;
-  if (s0 <= 0 || s0 % 4 != 0 || numel % s0 != 0) return false;
-  for (int v = 0; v < 4; ++v)
-    for (int d = 0; d < 3; ++d)
-      for (int k = 0; k < 3; ++k)
-        if (in.col_inl[(v * 3 + d) * 3 + k] != in.col_inl[v * 9] + d * s0 + k) return false;
-  const int64_t f0 = in.col_inl[0], P = in.col_inl[9] - f0;
-  if (f0 < 0 || P <= 0 || P % s0 != 0 || numel % P != 0) return false;
-  for (int v = 1; v < 4; ++v)
-    if (in.col_inl[v * 9] - f0 != v * P) return false;
-  const int64_t col = f0 % s0, row = (f0 % P) / s0, pl = f0 / P;  // halo column / first row / plane of var 0
-  if (col + nj + 1 >= s0 || pl + 4 > numel / P || P / s0 >= (1ll << 31) || numel / P >= (1ll << 31)) return false;
-  const int64_t c0 = col & ~int64_t(3);
-  a.al = (int32_t)(col - c0);
-  if (a.al > SM_BOX - SM_TW - 2 || a.al % 2 != 0) return false;  // 130 columns in the box, LDS.64 alignment
-  a.c0 = (int32_t)c0;
-  a.r0v = (int32_t)row;
-  a.p0v = (int32_t)pl;
-  *plane = P;
-  return true;
-}
-
 // tf32 (round to nearest even, 10 mantissa bits) bits of a finite f32
 uint32_t sm_tf32(float f) {
   uint32_t u;
@@ -403,8 +349,13 @@ template <int NT1, int ACT1, bool G4>
 int launch_sm(const smlrt_model_s& m, const DevPlan& in, const void* src, const DevPlan& out, void* dst,
               int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   SmArgs a{};
-  int64_t P = 0;
-  if (!stencil_shape(in, a, &P)) return SMLRT_E_UNSUPPORTED;
+  StencilGeom geo;
+  if (!stencil_geom(in, SM_BOX - SM_TW - 2, &geo)) return SMLRT_E_UNSUPPORTED;
+  const int64_t P = geo.plane;
+  a.c0 = geo.c0;
+  a.r0v = geo.r0v;
+  a.p0v = geo.p0v;
+  a.al = geo.al;
   const int64_t nj = (int64_t)in.sdiv[1].d, s0 = in.ustride[0];
   if (r0 % nj != 0 || (r1 % nj != 0 && r1 != in.n_rows)) return SMLRT_E_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(src) & 15) != 0) return SMLRT_E_UNSUPPORTED;
