@@ -2,6 +2,7 @@
 // Dispatch only: validation, device tables, and the choice of kernel.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -351,9 +352,18 @@ static int region_launch(smlrt_plan_t pin, const void* const* in_ptrs, const int
     if (m->precision == SMLRT_BF16)
       rc = launch_region_tc(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt,
                             pout->n_arrays, r0, r1, staged, s, status, false);
-    else
-      rc = launch_region_exact_fused(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt,
-                                     pout->n_arrays, r0, r1, staged, s, status, false);
+    else {
+      // the halo-stencil shape (C5): TMA-fed exact kernel; SMLRT_STENCIL_EXACT=0 (A/B) skips it
+      static const bool sx_on = [] {
+        const char* e = std::getenv("SMLRT_STENCIL_EXACT");
+        return !(e && e[0] == '0');
+      }();
+      if (sx_on)
+        rc = launch_region_stencil_exact(*m, din, in_ptrs, in_dt, dout, out_ptrs, out_dt, r0, r1, staged, s, status);
+      if (rc == SMLRT_E_UNSUPPORTED)
+        rc = launch_region_exact_fused(*m, din, in_ptrs, in_dt, pin->n_arrays, dout, out_ptrs, out_dt,
+                                       pout->n_arrays, r0, r1, staged, s, status, false);
+    }
     if (rc != SMLRT_OK && rc != SMLRT_E_UNSUPPORTED) return rc;
     if (rc == SMLRT_E_UNSUPPORTED && m->precision == SMLRT_BF16)
       return rc;  // launch_region_chain's message: the model has non-dense or > 4096-wide layers

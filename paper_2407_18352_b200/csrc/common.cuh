@@ -241,6 +241,10 @@ int small_mma_pack(smlrt_model_s& m);
 int launch_region_small_mma(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
                             const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
                             int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
+int launch_region_stencil_exact(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
+                                const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs,
+                                const int32_t* out_dt, int64_t r0, int64_t r1, float* staged, cudaStream_t s,
+                                uint32_t* status);
 int launch_region_stencil_tc(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
                              const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
                              int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);

@@ -122,3 +122,26 @@ def test_sharded_runtimes_cover_the_sweep(cuda, tmp_path):
             rt.invoke_region(rt.register_region(wl.descriptor(str(tmp_path / "m"))))
     want, _ = c_oracle.mlp_f32(wl.layers, wl.arrays["recs"])
     assert wl.buffers["price"].to_numpy().tobytes() == want[:, 0].tobytes()
+
+
+@pytest.mark.parametrize("nz,commit,launches", [(132, "fused", 1), (132, "checked", 2), (130, "fused", 1),
+                                                (66, "fused", 1)])
+def test_weather_exact_kernels_bitwise(cuda, tmp_path, nz, commit, launches):
+    """The TMA-ring exact stencil kernel (16-B multiple row pitch: 132, 66 is
+    not -> the per-point fused kernel) and the per-point kernel (pitch 130)
+    are both the oracle bit for bit, under both commits."""
+    nx = 37
+    wl = workloads.make("miniweather", (nx - 2) * (nz - 2))
+    st = np.stack([workloads._bumps(nx, nz, k) for k in range(4)]).astype(np.float32)
+    wl.arrays = {"state": st, "state_new": np.zeros_like(st)}
+    wl.env = {"NX": nx, "NZ": nz}
+    wl.to_device()
+    n0 = _native.launch_count()
+    run_region(wl, tmp_path, commit=commit)
+    assert _native.launch_count() - n0 == launches
+    fi, fo, ti, to = wl.functors()
+    x = oracle.gather(fi, ti, st.reshape(-1), st.shape, (nx * nz, nz, 1)).reshape(-1, 36)
+    y, _ = c_oracle.mlp_f32(wl.layers, x)
+    want = np.zeros_like(st)
+    want[:, 1:-1, 1:-1] = y.reshape(nx - 2, nz - 2, 4).transpose(2, 0, 1)
+    assert wl.buffers["state_new"].to_numpy().reshape(st.shape).tobytes() == want.tobytes()
