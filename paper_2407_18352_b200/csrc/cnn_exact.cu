@@ -337,10 +337,17 @@ __global__ void __launch_bounds__(256) conv_pool_k8oc8_kernel(const __grid_const
 // with TC = 8 a thread's columns are two groups of four, [4 tj, +4) and
 // [64 + 4 tj, +4), so each group's float4 reads are contiguous across threads
 constexpr int PJ = 128, PK = 32, TC = SMLRT_PF_TC;
-constexpr int PR = 4 * (256 / (PJ / TC));
+// PT threads per CTA (8 warps: 64-row tiles).  Measured on C4: 7 warps
+// (56-row tiles, 293 CTAs for the 296 slots of 2 per SM instead of 256 CTAs)
+// is equal (0.2763 vs 0.2771 ms region), so the CTA count is not the limiter
+#ifndef SMLRT_PF_PT
+#define SMLRT_PF_PT 256
+#endif
+constexpr int PT = SMLRT_PF_PT;
+constexpr int PR = 4 * (PT / (PJ / TC));
 
 template <bool FUSE2>
-__global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict__ x, int64_t rows, int in, int out,
+__global__ void __launch_bounds__(PT) dense_pair_kernel(const float* __restrict__ x, int64_t rows, int in, int out,
                                                          const float* __restrict__ W, const float* __restrict__ b,
                                                          int act, float* __restrict__ y, uint32_t* status,
                                                          const float* __restrict__ W2, const float* __restrict__ b2,
@@ -362,20 +369,20 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
 #pragma unroll
     for (int p = 0; p < TC / 2; ++p) acc[i][p] = 0ull;
   // the next K tile is fetched into registers while the current one is consumed
-  constexpr int NX = PR * PK / 256, NW = PJ * PK / 256;
+  constexpr int NX = (PR * PK + PT - 1) / PT, NW = (PJ * PK + PT - 1) / PT;
   float px[NX], pw[NW];
   auto fetch = [&](int k0) {
     const int kn = min(PK, in - k0);
 #pragma unroll
     for (int u = 0; u < NX; ++u) {
-      const int i = threadIdx.x + 256 * u, r = i / PK, k = i % PK;
+      const int i = threadIdx.x + PT * u, r = i / PK, k = i % PK;
       const int64_t gr = row0 + r;
-      px[u] = (gr < rows && k < kn) ? x[gr * in + k0 + k] : 0.0f;
+      px[u] = (i < PR * PK && gr < rows && k < kn) ? x[gr * in + k0 + k] : 0.0f;
     }
 #pragma unroll
     for (int u = 0; u < NW; ++u) {
-      const int i = threadIdx.x + 256 * u, j = i / PK, k = i % PK;
-      pw[u] = (j0 + j < out && k < kn) ? __ldg(W + (int64_t)(j0 + j) * in + k0 + k) : 0.0f;
+      const int i = threadIdx.x + PT * u, j = i / PK, k = i % PK;
+      pw[u] = (i < PJ * PK && j0 + j < out && k < kn) ? __ldg(W + (int64_t)(j0 + j) * in + k0 + k) : 0.0f;
     }
   };
   fetch(0);
@@ -383,13 +390,13 @@ __global__ void __launch_bounds__(256) dense_pair_kernel(const float* __restrict
     const int kn = min(PK, in - k0);
 #pragma unroll
     for (int u = 0; u < NX; ++u) {
-      const int i = threadIdx.x + 256 * u;
-      xs[i % PK][i / PK] = px[u];
+      const int i = threadIdx.x + PT * u;
+      if (i < PR * PK) xs[i % PK][i / PK] = px[u];
     }
 #pragma unroll
     for (int u = 0; u < NW; ++u) {
-      const int i = threadIdx.x + 256 * u;
-      wsh[i % PK][i / PK] = pw[u];
+      const int i = threadIdx.x + PT * u;
+      if (i < PJ * PK) wsh[i % PK][i / PK] = pw[u];
     }
     __syncthreads();
     if (k0 + PK < in) fetch(k0 + PK);
@@ -536,7 +543,7 @@ int dense_tail(const smlrt_model_s& m, int first, const float* cur, int64_t rows
       m.layers[first].out <= PJ && m.layers[first + 1].out <= 4) {
     const DevLayer &L1 = m.layers[first], &L2 = m.layers[first + 1];
     dim3 grid((unsigned)((rows + PR - 1) / PR), 1);
-    dense_pair_kernel<true><<<grid, 256, 0, s>>>(cur, rows, L1.in, L1.out, L1.w, L1.b, L1.act, y, status, L2.w, L2.b,
+    dense_pair_kernel<true><<<grid, PT, 0, s>>>(cur, rows, L1.in, L1.out, L1.w, L1.b, L1.act, y, status, L2.w, L2.b,
                                                   L2.out, L2.act, one2());
     count_launch();
     SMLRT_CUDA(cudaGetLastError());
@@ -566,7 +573,7 @@ int launch_dense_exact_tiled(const float* x, int64_t rows, const DevLayer& L, fl
   if (rows <= 0) return SMLRT_OK;
   if (L.kind != SMLRT_DENSE) return fail(SMLRT_E_UNSUPPORTED, "layer order not supported by the exact path");
   dim3 grid((unsigned)((rows + PR - 1) / PR), (unsigned)((L.out + PJ - 1) / PJ));
-  dense_pair_kernel<false><<<grid, 256, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status, nullptr, nullptr, 0,
+  dense_pair_kernel<false><<<grid, PT, 0, s>>>(x, rows, L.in, L.out, L.w, L.b, L.act, y, status, nullptr, nullptr, 0,
                                                 SMLRT_IDENTITY, one2());
   count_launch();
   SMLRT_CUDA(cudaGetLastError());

@@ -10,6 +10,4 @@ build_var() {
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v "$@" -c $src -o build_var/$name/${src%.cu}.o 2> build_var/$name/ptxas.txt || (cat build_var/$name/ptxas.txt; false)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libsmlrt_var_$name.so build_var/$name/*.o -lcudart
 }
-build_var rpt4 stencil_exact.cu -DSX_RPT_=4 -DSX_MINB=3
-build_var mb5 stencil_exact.cu -DSX_MINB=5
-build_var mb6 stencil_exact.cu -DSX_MINB=6
+build_var pt256 cnn_exact.cu -DSMLRT_PF_PT=256
