@@ -83,7 +83,10 @@ __device__ __forceinline__ int64_t smm_row(const DevPlan& P, int64_t r) {
   else return row_offset_uniform(P, (uint32_t)r);
 }
 
-template <int N1, int N2, int ACT1, int ACT2, bool ONE_D>
+// DENSE: packed AoS input rows (row pitch == F, columns contiguous): a warp
+// reads its tile's 16 x F floats as one coalesced run into shared memory and
+// each lane picks its fragment elements there -- no per-element addressing
+template <int N1, int N2, int ACT1, int ACT2, bool ONE_D, bool DENSE>
 __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ SmmArgs<N1, N2> a,
                                                         const __grid_constant__ DevPlan P,
                                                         const __grid_constant__ DevPlan Q,
@@ -139,6 +142,33 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
 
   auto in_off = [&](int64_t r) { return ONE_D ? r * ip : row_offset_uniform(P, (uint32_t)r); };
   auto out_off = [&](int64_t r) { return stg || ONE_D ? r * op : row_offset_uniform(Q, (uint32_t)r); };
+  __shared__ float xt[4][16 * 8];  // per-warp tile staging (DENSE)
+  float* xw = xt[threadIdx.x >> 5];
+  const float* dsrc = a.src + (DENSE ? P.col_inl[0] : 0);
+  // full tiles (all 16 rows in the call) load and store without predicates
+  const int64_t nfull = (a.r1 - a.r0) / 16;
+  auto load_dense = [&](int64_t tile, float (&v)[4]) {
+    const float* base = dsrc + (a.r0 + tile * 16) * F + lane;
+    if (tile < nfull) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (32 * u < 16 * 7 && lane + 32 * u < 16 * F) ? __ldg(base + 32 * u) : 0.0f;
+    } else {
+      const int64_t left = tile < ntiles ? (a.r1 - a.r0 - tile * 16) * F : 0;  // elements in the tail tile
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (lane + 32 * u < 16 * F && lane + 32 * u < left) ? __ldg(base + 32 * u) : 0.0f;
+    }
+  };
+  auto frag_dense = [&](const float (&v)[4], uint32_t (&a1)[4]) {
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lane + 32 * u < 16 * F) xw[lane + 32 * u] = v[u];
+    __syncwarp();
+    a1[0] = k0ok ? __float_as_uint(xw[g * F + q]) : c0v;
+    a1[1] = k0ok ? __float_as_uint(xw[(g + 8) * F + q]) : c0v;
+    a1[2] = k1ok ? __float_as_uint(xw[g * F + q + 4]) : c1v;
+    a1[3] = k1ok ? __float_as_uint(xw[(g + 8) * F + q + 4]) : c1v;
+  };
   auto load = [&](int64_t tile, uint32_t (&a1)[4]) {
     const int64_t ra = a.r0 + tile * 16 + g, rb = ra + 8;
     const bool va = tile < ntiles && ra < a.r1, vb = tile < ntiles && rb < a.r1;
@@ -151,10 +181,18 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
     a1[3] = vb && k1ok ? __float_as_uint(__ldg(pb + c1)) : c1v;
   };
   uint32_t nxt[4];
-  load(wid, nxt);
+  float nxv[4];
+  if constexpr (DENSE) load_dense(wid, nxv);
+  else load(wid, nxt);
   for (int64_t tile = wid; tile < ntiles; tile += nw) {
-    const uint32_t a1[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
-    load(tile + nw, nxt);
+    uint32_t a1[4];
+    if constexpr (DENSE) {
+      frag_dense(nxv, a1);
+      load_dense(tile + nw, nxv);
+    } else {
+      a1[0] = nxt[0], a1[1] = nxt[1], a1[2] = nxt[2], a1[3] = nxt[3];
+      load(tile + nw, nxt);
+    }
     float d1[T1][4];
 #pragma unroll
     for (int t = 0; t < T1; ++t) {
@@ -193,13 +231,20 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
     // y = (row g: outputs o0, o1), (row g + 8: o0, o1); unused columns and
     // rows past the end are finite (zero inputs, zero weights)
     const int64_t ra = a.r0 + tile * 16 + g, rb = ra + 8;
-    const bool va = ra < a.r1, vb = rb < a.r1;
-    float* pa = obase + out_off(va ? ra : a.r0);
-    float* pb = obase + out_off(vb ? rb : a.r0);
-    if (va && h0) pa[oc0] = y[0];
-    if (va && h1) pa[oc1] = y[1];
-    if (vb && h0) pb[oc0] = y[2];
-    if (vb && h1) pb[oc1] = y[3];
+    if ((stg || ONE_D) && tile < nfull) {
+      float* pa = obase + ra * op;
+      float* pb = pa + 8 * op;
+      if (h0) pa[oc0] = y[0], pb[oc0] = y[2];
+      if (h1) pa[oc1] = y[1], pb[oc1] = y[3];
+    } else {
+      const bool va = ra < a.r1, vb = rb < a.r1;
+      float* pa = obase + out_off(va ? ra : a.r0);
+      float* pb = obase + out_off(vb ? rb : a.r0);
+      if (va && h0) pa[oc0] = y[0];
+      if (va && h1) pa[oc1] = y[1];
+      if (vb && h0) pb[oc0] = y[2];
+      if (vb && h1) pb[oc1] = y[3];
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) chk = fmaf(y[e], 0.0f, chk);
   }
@@ -307,15 +352,18 @@ int launch_smm(const smlrt_model_s& m, const DevPlan& in, const void* src, const
     int dev_id = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id);
-    SMLRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_mma_kernel<N1, N2, ACT1, ACT2, true>, 128, 0));
+    SMLRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_mma_kernel<N1, N2, ACT1, ACT2, true, false>, 128, 0));
     slots = std::max(1, per_sm) * sms;
   }
   const int64_t blocks = std::min<int64_t>((tiles + 3) / 4, slots);
   const unsigned grid = (unsigned)std::max<int64_t>(1, blocks);
-  if (in.n_sweep == 1 && out.n_sweep == 1)
-    small_mma_kernel<N1, N2, ACT1, ACT2, true><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
+  const bool dense = in.n_sweep == 1 && in.dense_rows && in.ustride[0] == in.n_cols;
+  if (in.n_sweep == 1 && out.n_sweep == 1 && dense)
+    small_mma_kernel<N1, N2, ACT1, ACT2, true, true><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
+  else if (in.n_sweep == 1 && out.n_sweep == 1)
+    small_mma_kernel<N1, N2, ACT1, ACT2, true, false><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
   else
-    small_mma_kernel<N1, N2, ACT1, ACT2, false><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
+    small_mma_kernel<N1, N2, ACT1, ACT2, false, false><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
   count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
