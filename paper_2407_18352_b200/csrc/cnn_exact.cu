@@ -597,25 +597,6 @@ int infer_cnn_dense(const smlrt_model_s& m, const float* x, int64_t rows, float*
   return rc;
 }
 
-namespace {
-// per device: a lowest-priority stream for the conv fronts and a
-// highest-priority stream for the dense tails of the overlapped CNN region
-// (the block scheduler hands freed SM slots to the dense tail's CTAs first)
-cudaStream_t cnn_stream(int dev, int which) {
-  static std::mutex mu;
-  static cudaStream_t st[64][2] = {};
-  std::lock_guard<std::mutex> g(mu);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!st[dev][which]) {
-    int least = 0, greatest = 0;
-    cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (cudaStreamCreateWithPriority(&st[dev][which], cudaStreamNonBlocking, which ? greatest : least) != cudaSuccess)
-      st[dev][which] = nullptr;
-  }
-  return st[dev][which];
-}
-}  // namespace
-
 // bf16 CNN region (precision "bf16"): the conv(+pool) front is the exact
 // CUDA-core kernel (it is HBM-bound: its FP32 work fits under the window
 // reads), writing its features as bf16 rows padded to the chain's K; the
@@ -661,85 +642,38 @@ int launch_region_cnn_bf16(const smlrt_model_s& m, const DevPlan& in, const void
   return rc;
 }
 
-// Rows are processed in chunks of <= 16384 on the caller's stream.
-// SMLRT_CNN_CHUNKS=k > 1 (experiment, off): k chunks, each with its own
-// feature buffer; the conv fronts (HBM-bound) run in order on a low-priority
-// stream, the dense tail + scatter of chunk c (FP32-bound) on a high-priority
-// stream as soon as front c is done, so the tail of c may co-run with the
-// front of c+1.  Measured on C4 (16,384 windows, region ms): 1 / 2 / 4 / 8 /
-// 16 chunks -> 0.324 / 0.354 / 0.402 / 0.640 / 1.162: a chunk's dense tail
-// is a 64-rows-per-CTA grid too small to spread over the SMs the fronts
-// leave, so it serialises.
+// Rows are processed in chunks of <= 16384 on the caller's stream: conv
+// front, dense tail, scatter.  (Round 2 measured an overlapped variant --
+// fronts on a low-priority stream, each chunk's tail on a high-priority one --
+// at 0.354 / 0.402 / 0.640 ms for 2 / 4 / 8 chunks vs 0.324 ms in one chunk:
+// a chunk's tail grid is too small to fill the SMs the fronts leave; removed.)
 int launch_region_cnn(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs, const int32_t* in_dt,
                       int n_in, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt, int n_out,
                       int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status) {
   if (!in.uniform) return fail(SMLRT_E_UNSUPPORTED, "CNN region needs a single-array input map");
   if (m.precision == SMLRT_BF16)
     return launch_region_cnn_bf16(m, in, in_ptrs, in_dt, out, out_ptrs, out_dt, n_out, r0, r1, staged, s, status);
-  static const int n_chunks = [] {
-    const char* e = std::getenv("SMLRT_CNN_CHUNKS");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? v : 1;
-  }();
   const int64_t rows = r1 - r0;
   if (rows <= 0) return SMLRT_OK;
-  const int64_t ch = n_chunks > 1 ? std::max<int64_t>(1024, (rows + n_chunks - 1) / n_chunks)
-                                  : std::min<int64_t>(16384, rows);
-  const bool overlap = n_chunks > 1 && rows > ch;
-  const int64_t nb = overlap ? (rows + ch - 1) / ch : 1;  // feature buffers (one per chunk when overlapped)
+  const int64_t ch = std::min<int64_t>(16384, rows);
   size_t per = 1;  // widest activation after the conv front
   for (int l = 1; l < m.n_layers; ++l) per = std::max(per, (size_t)m.layers[l].out);
-  const size_t slot = per * 3 + m.out_features;  // f, t0, t1, y per row
   float* buf;
-  SMLRT_CUDA(cudaMallocAsync(&buf, slot * ch * 4 * nb, s));
-  int dev = 0;
-  SMLRT_CUDA(cudaGetDevice(&dev));
-  cudaStream_t sa = overlap ? cnn_stream(dev, 0) : s;
-  cudaStream_t sb = overlap ? cnn_stream(dev, 1) : s;
-  if (!sa || !sb) sa = sb = s;
-  std::vector<cudaEvent_t> ev;
-  auto event = [&]() {
-    cudaEvent_t e = nullptr;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    ev.push_back(e);
-    return e;
-  };
-  if (sa != s) {
-    cudaEvent_t e0 = event();
-    SMLRT_CUDA(cudaEventRecord(e0, s));
-    SMLRT_CUDA(cudaStreamWaitEvent(sa, e0, 0));
-    SMLRT_CUDA(cudaStreamWaitEvent(sb, e0, 0));
-  }
+  SMLRT_CUDA(cudaMallocAsync(&buf, (per * 3 + m.out_features) * ch * 4, s));
+  float* f = buf;  // front output, two ping-pong activations, outputs
+  float* t0 = f + per * ch;
+  float* t1 = t0 + per * ch;
+  float* yo = t1 + per * ch;
   int rc = SMLRT_OK;
-  int c = 0;
-  for (int64_t r = r0; r < r1 && !rc; r += ch, ++c) {
+  for (int64_t r = r0; r < r1 && !rc; r += ch) {
     const int64_t n = std::min(ch, r1 - r);
-    float* f = buf + slot * ch * (c % nb);
-    float* t0 = f + per * ch;
-    float* t1 = t0 + per * ch;
-    float* yo = t1 + per * ch;
     int ow, nl;
-    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, sa);
+    rc = launch_front(m, nullptr, &in, in_ptrs[in.uarray], in_dt[in.uarray], r, r + n, f, &ow, &nl, s);
     if (rc) break;
-    if (sa != sb) {
-      cudaEvent_t e = event();
-      SMLRT_CUDA(cudaEventRecord(e, sa));
-      SMLRT_CUDA(cudaStreamWaitEvent(sb, e, 0));
-    }
     float* ydst = staged ? staged + (r - r0) * m.out_features : yo;
-    rc = dense_tail(m, nl, f, n, ydst, t0, t1, sb, status);
-    if (rc) break;
-    if (!staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, sb, nullptr);
+    rc = dense_tail(m, nl, f, n, ydst, t0, t1, s, status);
+    if (!rc && !staged) rc = launch_scatter(out, ydst, SMLRT_F32, out_ptrs, out_dt, n_out, r, r + n, s, nullptr);
   }
-  if (sa != s) {
-    // the caller's stream continues after both side streams' work
-    cudaEvent_t ea = event(), eb = event();
-    cudaEventRecord(ea, sa);
-    cudaEventRecord(eb, sb);
-    cudaStreamWaitEvent(s, ea, 0);
-    cudaStreamWaitEvent(s, eb, 0);
-  }
-  for (auto& e : ev) cudaEventDestroy(e);
   cudaFreeAsync(buf, s);
   (void)n_in;
   return rc;

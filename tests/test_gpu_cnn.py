@@ -66,26 +66,17 @@ def test_cnn_full_size_subsample(cuda, tmp_path):
     assert got[idx].tobytes() == want.tobytes()
 
 
-def test_cnn_overlapped_chunks_bitwise(cuda):
-    """The opt-in two-stream chunked CNN region (SMLRT_CNN_CHUNKS=3: conv
-    front on a side stream, dense tail on the caller's) is bitwise the oracle,
-    including a ragged last chunk (run in a subprocess: the switch is read once)."""
-    import os
-    import subprocess
-    import sys
-    code = ("import sys, pathlib, tempfile, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
-            "import paper_2407_18352_b200 as sm; from paper_2407_18352_b200 import workloads; from oracle import oracle;"
-            "n = 3 * 4096 + 123; wl = workloads.make('particlefilter', n); wl.to_device();"
-            "d = pathlib.Path(tempfile.mkdtemp()); sm.save_model(wl.model, d / 'pf');"
-            "rt = sm.Runtime(); rt.invoke_region(rt.register_region(wl.descriptor(str(d / 'pf'))));"
-            "got = wl.buffers['locs'].to_numpy(); idx = np.r_[0:50, 4090:4100, 8190:8200, n - 130:n];"
-            "x = wl.arrays['frames'][idx, 16:144, 16:144].reshape(len(idx), -1);"
-            "want, _ = oracle.cnn_forward(workloads.cnn_layers(), x, (1, 128, 128));"
-            "assert got[idx].tobytes() == want.tobytes(); print('ok')")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "SMLRT_CNN_CHUNKS": "3"},
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+def test_cnn_region_chunks_bitwise(cuda, tmp_path):
+    """More frames than one 16,384-row chunk: the region runs chunk by chunk,
+    bitwise the oracle across the chunk boundary."""
+    n = 16384 + 123
+    wl = workloads.make("particlefilter", n)
+    wl.to_device()
+    got = run(wl, tmp_path)
+    idx = np.r_[0:40, 16360:16400, n - 40:n]
+    x = wl.arrays["frames"][idx, 16:144, 16:144].reshape(len(idx), -1)
+    want, _ = oracle.cnn_forward(workloads.cnn_layers(), x, (1, 128, 128))
+    assert got[idx].tobytes() == want.tobytes()
 
 
 # --------------------------------------------------------------- bf16 CNN --
