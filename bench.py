@@ -146,11 +146,21 @@ def spawn_ranks(n: int) -> int:
     return max(p.wait() for p in procs)
 
 
+# SMLRT_BENCH_SHARED_GPU=1 (diagnostic): every rank on cuda:0 with gloo
+# collectives -- exercises the N > 1 code paths (weak/strong shards, the
+# MiniWeather slab stepper, max-over-ranks timing) on a one-GPU box; never a
+# scaling number
+SHARED_GPU = os.environ.get("SMLRT_BENCH_SHARED_GPU") == "1"
+
+
 def dist_setup(backend="nccl"):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARED_GPU and backend == "nccl":
+        backend, local = "gloo", 0
+        torch.cuda.set_device(0)
     if world > 1:
         import torch.distributed as dist
         if backend == "nccl":
@@ -171,7 +181,8 @@ def max_over_ranks(x: float, world: int, device=None) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device if device is not None else "cpu")
+    on_dev = device is not None and dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=device if on_dev else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -569,7 +580,7 @@ def measure_halo(args, rank, world, local, dev, headline, pk, pk_src, fp32_peak,
         # exchange is collective); rank 0's slab interior vs the unsharded oracle
         from oracle import oracle
         fresh = halo.Slab.from_global(state, world, rank, dev)
-        st2 = halo.SlabStepper(fresh, mdir, runtime=rt, exchange=halo.HaloExchange())
+        st2 = halo.SlabStepper(fresh, mdir, runtime=rt, exchange=halo.HaloExchange(), name="mw_parity")
         st2.step()
     if rank == 0 and not args.no_parity:
         got = st2.interior()

@@ -112,6 +112,17 @@ class HaloExchange:
             rcv = self._tmp("r_dn", s[:, R + 1, :])
             ops += [dist.P2POp(dist.isend, snd, r + 1, self.group), dist.P2POp(dist.irecv, rcv, r + 1, self.group)]
             back.append((s[:, R + 1, :], rcv))
+        if ops and dist.get_backend(self.group) == "gloo" and s.is_cuda:
+            # gloo moves host tensors: stage the halo rows through the host
+            host = [op.tensor.cpu() if op.op is dist.isend else torch.empty(op.tensor.shape, dtype=op.tensor.dtype)
+                    for op in ops]
+            ops = [dist.P2POp(op.op, h, op.peer, self.group) for op, h in zip(ops, host)]
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            recvd = [h for op, h in zip(ops, host) if op.op is dist.irecv]
+            for (dst, _), h in zip(back, recvd):
+                dst.copy_(h)
+            return
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
@@ -136,14 +147,14 @@ class LocalExchange:
 class SlabStepper:
     """Time-steps one slab with the ml(infer) region on the B200 runtime.
 
-    Two region descriptors (cur -> nxt and nxt -> cur) are registered once, so
-    plans and the model stay cached across steps; `step()` = exchange +
-    invoke + swap.  `region_fn(slab)` replaces the invoke for tests that step
+    Two region descriptors (cur -> nxt and nxt -> cur) are registered once
+    (names `{name}{rank}_{0,1}`: unique per Runtime), so plans and the model
+    stay cached across steps; `step()` = exchange + invoke + swap.  `region_fn(slab)` replaces the invoke for tests that step
     with the CPU oracle (no CUDA device)."""
 
     def __init__(self, slab: Slab, model_path: str, runtime: Optional[Runtime] = None,
                  exchange: Optional[HaloExchange] = None,
-                 region_fn: Optional[Callable[[Slab], None]] = None):
+                 region_fn: Optional[Callable[[Slab], None]] = None, name: str = "mw_slab"):
         self.slab = slab
         self.exchange = exchange
         self.region_fn = region_fn
@@ -162,7 +173,7 @@ class SlabStepper:
             ml = parse_directive(f'ml(infer) in(state) out(state_new) model("{model_path}")')
             for k in range(2):
                 desc = RegionDescriptor(
-                    name=f"mw_slab{slab.rank}_{k}", accurate_fn=lambda: None, ml=ml,
+                    name=f"{name}{slab.rank}_{k}", accurate_fn=lambda: None, ml=ml,
                     in_maps=[BoundMap(f_in, t_in, bufs[k])], out_maps=[BoundMap(f_out, t_out, bufs[1 - k])],
                     env=env)
                 self._handles.append(runtime.register_region(desc))

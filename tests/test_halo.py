@@ -143,3 +143,25 @@ def test_gpu_slabs_match_oracle(cuda, tmp_path, world):
                 st.step()
         for s, st in zip(slabs, steppers):
             assert np.array_equal(st.interior(), want[:, s.g0:s.g1]), s.rank
+
+
+@pytest.mark.gpu
+def test_gpu_two_steppers_share_a_runtime(cuda, tmp_path):
+    """A second stepper over the same rank's slab (the bench's one-step parity
+    check next to the timed stepper) registers its own regions: names are
+    per stepper, so one Runtime holds both (a shared name would raise
+    DuplicateRegionError, as the reference's registry does)."""
+    import paper_2407_18352_b200 as sm
+    from paper_2407_18352_b200.errors import DuplicateRegionError
+    field, layers = _field(), _layers()
+    want = _reference_trajectory(field, layers, 1)
+    sm.save_model(sm.Model(36, 4, [sm.DenseLayer(w, b, a) for w, b, a in layers]), tmp_path / "m")
+    with sm.Runtime() as rt:
+        sa, sb = halo.Slab.from_global(field, 1, 0, cuda), halo.Slab.from_global(field, 1, 0, cuda)
+        a = halo.SlabStepper(sa, str(tmp_path / "m"), runtime=rt)
+        b = halo.SlabStepper(sb, str(tmp_path / "m"), runtime=rt, name="mw_parity")
+        for st, s in ((a, sa), (b, sb)):
+            st.step()
+            assert np.array_equal(st.interior(), want[:, s.g0:s.g1])
+        with pytest.raises(DuplicateRegionError):
+            halo.SlabStepper(halo.Slab.from_global(field + 1, 1, 0, cuda), str(tmp_path / "m"), runtime=rt)
