@@ -140,15 +140,24 @@ def _ns_since(t0: int) -> int:
     return max(time.perf_counter_ns() - t0, 1)
 
 
-def _shard_rows(n_rows: int, shard) -> tuple[int, int]:
+def _shard_rows(n_rows: int, shard, inner: int = 1) -> tuple[int, int]:
+    """Flattened sweep rows [r0, r1) of a shard: sweep axis 0 split into
+    contiguous blocks; `inner` = product of the other sweep
+    extents, so a shard of a 2-D sweep is whole rows of the grid."""
     if shard is None:
         return 0, n_rows
     rank, world = shard
-    per = -(-n_rows // world)
-    return min(rank * per, n_rows), min((rank + 1) * per, n_rows)
+    a0 = n_rows // inner
+    per = -(-a0 // world)
+    return min(rank * per, a0) * inner, min((rank + 1) * per, a0) * inner
 
 
-def gather_rows_to_root(local: torch.Tensor, n_rows: int, shard, root: int = 0, group=None):
+def _inner_of(plan) -> int:
+    """product of the sweep extents after axis 0 (1 for a 1-D sweep)"""
+    return int(np.prod(plan.sweep[1:], dtype=np.int64)) if plan.sweep is not None and len(plan.sweep) > 1 else 1
+
+
+def gather_rows_to_root(local: torch.Tensor, n_rows: int, shard, root: int = 0, group=None, inner: int = 1):
     """Concatenate every rank's block of sweep rows (`_shard_rows` order) on
     `root`: the collect snapshots of a sharded region go to the one rank that
     holds the SRDB writer lock (srdb.py:116-126), SURVEY.md 8(e).  `local` is
@@ -157,7 +166,7 @@ def gather_rows_to_root(local: torch.Tensor, n_rows: int, shard, root: int = 0, 
     Returns the [n_rows, F] tensor on root, None elsewhere."""
     import torch.distributed as dist
     rank, world = shard
-    per = -(-n_rows // world)
+    per = -(-(n_rows // inner) // world) * inner  # the largest block (_shard_rows)
     if dist.get_backend(group) == "gloo" and local.is_cuda:
         local = local.cpu()  # gloo gathers host tensors (NCCL moves device tensors directly)
     buf = local
@@ -447,7 +456,9 @@ class Runtime:
         for m, d in zip(desc.in_maps + desc.inout_maps, in_maps):
             self._staging.upload(m.array, d.array)
         n_rows = self._plans_rows(in_maps)
-        rows = _shard_rows(n_rows, self.shard)
+        sweep = self._sweep_of(in_maps)
+        inner = int(np.prod(sweep[1:], dtype=np.int64)) if len(sweep) > 1 else 1
+        rows = _shard_rows(n_rows, self.shard, inner)
         x_loc = self._gather_dense(in_maps, rows=rows).data
         self._sync()
         map_to = _ns_since(t0)
@@ -459,8 +470,8 @@ class Runtime:
         for m, d in zip(desc.out_maps + desc.inout_maps, out_maps):
             self._staging.upload(m.array, d.array)
         y_loc = self._gather_dense(out_maps, rows=rows).data
-        x_all = gather_rows_to_root(x_loc, n_rows, self.shard, root=self.collect_root)
-        y_all = gather_rows_to_root(y_loc, n_rows, self.shard, root=self.collect_root)
+        x_all = gather_rows_to_root(x_loc, n_rows, self.shard, root=self.collect_root, inner=inner)
+        y_all = gather_rows_to_root(y_loc, n_rows, self.shard, root=self.collect_root, inner=inner)
         index = -1
         if rank == self.collect_root:
             xs = self._full_shape(in_maps, x_all)
@@ -611,7 +622,7 @@ class Runtime:
         for m, d in zip(host_out, out_maps):
             if not m.array.is_device and not (skip_ok and _covers(pout, d.array)):
                 self._staging.upload(m.array, d.array)
-        r0, r1 = _shard_rows(rows, self.shard)
+        r0, r1 = _shard_rows(rows, self.shard, _inner_of(pin))
         status = self._status_word()
         stream = torch.cuda.current_stream(self.device)
         map_to = _ns_since(t0)
@@ -706,7 +717,7 @@ class Runtime:
             return None
         if len(host_in) != 1 or len(host_out) != 1:
             return None
-        r0, r1 = _shard_rows(rows, self.shard)
+        r0, r1 = _shard_rows(rows, self.shard, _inner_of(pin))
         if r1 <= r0:
             return None
         if _shares_storage(pin, pout):

@@ -22,6 +22,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def test_shards_of_a_grid_are_whole_rows():
+    """A 2-D sweep shards along axis 0: every block is whole grid rows and the
+    blocks tile the sweep."""
+    rows0, inner = 4094, 2046
+    for world in (1, 2, 3, 8):
+        blocks = [_shard_rows(rows0 * inner, (r, world), inner) for r in range(world)]
+        assert blocks[0][0] == 0 and blocks[-1][1] == rows0 * inner
+        for (a0, a1), (b0, b1) in zip(blocks, blocks[1:]):
+            assert a1 == b0
+        assert all(a % inner == 0 and b % inner == 0 for a, b in blocks)
+
+
 def _worker(rank, world, port, n, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -73,13 +85,13 @@ def test_shard_rows_partition():
                 assert a1 == b0 and a0 <= a1
 
 
-def _gather_worker(rank, world, port, n, out):
+def _gather_worker(rank, world, port, n, out, inner=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2407_18352_b200.runtime import gather_rows_to_root
     full = torch.arange(n * 3, dtype=torch.float64).reshape(n, 3)
-    r0, r1 = _shard_rows(n, (rank, world))
-    got = gather_rows_to_root(full[r0:r1].clone(), n, (rank, world), root=world - 1)
+    r0, r1 = _shard_rows(n, (rank, world), inner)
+    got = gather_rows_to_root(full[r0:r1].clone(), n, (rank, world), root=world - 1, inner=inner)
     if rank == world - 1:
         out.put(got.numpy().tobytes())
     else:
@@ -87,14 +99,14 @@ def _gather_worker(rank, world, port, n, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,world", [(7, 2), (1000, 3), (2, 3)])
-def test_collect_rows_meet_on_the_writer_rank(n, world):
+@pytest.mark.parametrize("n,world,inner", [(7, 2, 1), (1000, 3, 1), (2, 3, 1), (20, 3, 2), (130 * 10, 4, 130)])
+def test_collect_rows_meet_on_the_writer_rank(n, world, inner):
     """The collect snapshots of a sharded region (uneven last block, a rank
     with no rows) reassemble in sweep order on the writer rank."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n, q, inner)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=120)
