@@ -4,9 +4,9 @@
 // MMAs with the activations kept in registers.
 //
 // At bf16 such a model is 0.1 % of the tensor peak per byte it reads, so the
-// region is HBM- and latency-bound: a warp owns 16-row tiles, its lanes load
-// their A-fragment elements of the tile's rows straight from the application
-// array through the in-plan (tf32 m16n8k8 for layer 1: the f32 features are
+// region is HBM- and latency-bound: a warp owns 16-row tiles whose rows
+// arrive through a ring of bulk copies (packed AoS rows) or per-lane loads
+// through the in-plan (tf32 m16n8k8 for layer 1: the f32 features are
 // the operands), the bias is each accumulator's initial value, and act +
 // bf16 packing of layer l's accumulators IS layer l+1's A fragment (the m16n8
 // C and A fragment layouts coincide), so no activation ever leaves the
@@ -26,7 +26,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int SMM_G = 8;
+constexpr int SMM_G = 8, SMM_F = 8;
 
 template <int N1, int N2>
 struct SmmArgs {
@@ -39,29 +39,77 @@ struct SmmArgs {
 };
 
 // per-lane B fragments and biases, laid out [what][lane] in global memory and
-// staged through shared memory at kernel start
-// Biases ride in the MMAs: layer 1's input column F (< 8) is the constant 1
-// with b1 as its weights; layers 2 and 3 get one more k16 step whose A
-// fragment is the constant (1, 0, ...) and whose B fragment is the bias.
+// staged through shared memory at kernel start.  Each bias is its
+// accumulator's initial value (f32, the lane's output columns 2q, 2q + 1 of
+// an n8 tile -- the m16n8 C fragment holds them for rows g and g + 8).
 template <int N1, int N2>
 struct SmmFrags {
-  static constexpr int T1 = N1 / 8, T2 = N2 / 8, K2 = N1 / 16 + 1, K3 = N2 / 16 + 1;
-  uint32_t w1[T1][32][2];      // tf32 (k = q, q + 4; n = 8t + g), row F = b1
-  uint32_t w2[T2][K2][32][2];  // bf16 pairs; step K2-1 = b2
-  uint32_t w3[K3][32][2];      // step K3-1 = b3
+  static constexpr int T1 = N1 / 8, T2 = N2 / 8, K2 = N1 / 16, K3 = N2 / 16;
+  uint32_t w1[T1][32][2];      // tf32 (k = q, q + 4; n = 8t + g)
+  float4 b1[T1][32];           // C quad (n = 8t + 2q, 8t + 2q + 1) x rows g, g + 8
+  uint32_t w2[T2][K2][32][2];  // bf16 pairs
+  float4 b2[T2][32];
+  uint32_t w3[K3][32][2];
+  float4 b3[32];
 };
 
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+// dense input rows stream through a ring of shared-memory stages filled by
+// 1-D bulk copies: a chunk is SMM_TPW tiles per warp (the CTA's 4 warps), so
+// SMM_S - 1 chunks of every resident CTA are in flight while it computes --
+// per-lane loads one tile ahead keep too few bytes in flight to cover DRAM
+// latency at this little compute per byte
+#ifndef SMM_TPW
+#define SMM_TPW 4  // tiles per warp per chunk
+#endif
+#ifndef SMM_S
+#define SMM_S 4  // ring stages
+#endif
+#ifndef SMM_MINB
+#define SMM_MINB 1
+#endif
+constexpr int SMM_CH = 4 * SMM_TPW * 16;  // rows per chunk
+__host__ __device__ constexpr int smm_stage_floats(int F) { return (SMM_CH * F + 8 + 31) / 32 * 32; }
+
+// not volatile: the two tiles a warp holds interleave their MMA chains
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                         const float4& c) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c.x), "f"(c.y), "f"(c.z), "f"(c.w));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+// first k step of a chain: the accumulator starts at the bias quad
+__device__ __forceinline__ void mma_bf16_c(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                           const float4& c) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c.x), "f"(c.y), "f"(c.z), "f"(c.w));
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// bounded wait: a copy that never lands traps instead of hanging the device
+__device__ __forceinline__ void smm_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  for (uint32_t n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (n > (1u << 26)) __trap();
+  }
 }
 
 template <int ACT>
@@ -76,31 +124,34 @@ __device__ __forceinline__ float act_f(float y, int act) {
   return y;
 }
 
-// row offset of sweep row r: the 1-D sweep (AoS / SoA records) is one multiply
-template <bool ONE_D>
-__device__ __forceinline__ int64_t smm_row(const DevPlan& P, int64_t r) {
-  if constexpr (ONE_D) return r * P.ustride[0];
-  else return row_offset_uniform(P, (uint32_t)r);
-}
-
-// DENSE: packed AoS input rows (row pitch == F, columns contiguous): a warp
-// reads its tile's 16 x F floats as one coalesced run into shared memory and
-// each lane picks its fragment elements there -- no per-element addressing
+// DENSE: packed AoS input rows (row pitch == F, columns contiguous) stream
+// through the bulk-copy ring and each lane picks its fragment elements out of
+// the staged rows; the rows past the last whole chunk (and every non-dense
+// plan) load per lane through the plan, one tile ahead
 template <int N1, int N2, int ACT1, int ACT2, bool ONE_D, bool DENSE>
-__global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ SmmArgs<N1, N2> a,
+__global__ void __launch_bounds__(128, SMM_MINB) small_mma_kernel(const __grid_constant__ SmmArgs<N1, N2> a,
                                                         const __grid_constant__ DevPlan P,
                                                         const __grid_constant__ DevPlan Q,
                                                         const SmmFrags<N1, N2>* __restrict__ fr) {
   using Fr = SmmFrags<N1, N2>;
   constexpr int T1 = Fr::T1, T2 = Fr::T2, K2 = Fr::K2, K3 = Fr::K3;
   __shared__ __align__(16) Fr sf;
+  __shared__ __align__(8) uint64_t full[SMM_S];
+  extern __shared__ __align__(128) float ring[];
+  const int F = P.n_cols;
+  if constexpr (DENSE) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < SMM_S; ++s) mbar_init(&full[s], 1);
+      mbar_fence_init();
+    }
+  }
   {
     const uint4* s4 = reinterpret_cast<const uint4*>(fr);
     uint4* d4 = reinterpret_cast<uint4*>(&sf);
     for (int i = threadIdx.x; i < (int)(sizeof(Fr) / 16); i += blockDim.x) d4[i] = __ldg(s4 + i);
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3, warp = threadIdx.x >> 5;
   uint32_t w1[T1][2], w3[K3][2];
 #pragma unroll
   for (int t = 0; t < T1; ++t) w1[t][0] = sf.w1[t][lane][0], w1[t][1] = sf.w1[t][lane][1];
@@ -117,112 +168,63 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
 #endif
 #pragma unroll
   for (int k = 0; k < K3; ++k) w3[k][0] = sf.w3[k][lane][0], w3[k][1] = sf.w3[k][lane][1];
-  // A of the bias steps: (1, 0) at k = 0 of the step for quad member 0
-  const uint32_t one_lo = q == 0 ? 0x3f80u : 0u;  // bf16 1.0 in the low half
-  const uint32_t abias[4] = {one_lo, one_lo, 0u, 0u};
-  // this lane's feature columns (k = q and q + 4 of the padded 8; column F is
-  // the constant 1 of layer 1's bias) and the outputs it holds (2q, 2q + 1)
-  const int F = P.n_cols;
+  // this lane's feature columns (k = q and q + 4 of the padded 8) and the
+  // outputs it holds (2q, 2q + 1)
   const bool k0ok = q < F, k1ok = q + 4 < F;
-  const uint32_t c0v = q == F ? 0x3f800000u : 0u, c1v = q + 4 == F ? 0x3f800000u : 0u;
   const int64_t c0 = k0ok ? P.col_inl[q] : 0, c1 = k1ok ? P.col_inl[q + 4] : 0;
   const int o0 = 2 * q, o1 = 2 * q + 1;
   const bool h0 = o0 < a.g, h1 = o1 < a.g;
   const bool stg = a.staged != nullptr;
-  // per-lane pointers of the first tile's rows g and g + 8 (ONE_D: advanced by
-  // a constant per tile; otherwise recomputed through the plan)
   const int64_t ntiles = (a.r1 - a.r0 + 15) / 16;
-  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
   const int64_t ip = ONE_D ? P.ustride[0] : 0;  // input element step per row
   const int64_t op = stg ? a.g : (ONE_D ? Q.ustride[0] : 0);
   const int64_t oc0 = stg ? o0 : (h0 ? Q.col_inl[o0] : 0), oc1 = stg ? o1 : (h1 ? Q.col_inl[o1] : 0);
   float* const obase = stg ? a.staged - a.r0 * a.g : a.dst;
-  float chk = 0.0f;  // y * 0 accumulates NaN iff an output is non-finite
+  const int64_t nfull = (a.r1 - a.r0) / 16;  // tiles with all 16 rows in the call
+  float chk = 0.0f;                          // y * 0 accumulates NaN iff an output is non-finite
 
   auto in_off = [&](int64_t r) { return ONE_D ? r * ip : row_offset_uniform(P, (uint32_t)r); };
   auto out_off = [&](int64_t r) { return stg || ONE_D ? r * op : row_offset_uniform(Q, (uint32_t)r); };
-  __shared__ float xt[4][16 * 8];  // per-warp tile staging (DENSE)
-  float* xw = xt[threadIdx.x >> 5];
-  const float* dsrc = a.src + (DENSE ? P.col_inl[0] : 0);
-  // full tiles (all 16 rows in the call) load and store without predicates
-  const int64_t nfull = (a.r1 - a.r0) / 16;
-  auto load_dense = [&](int64_t tile, float (&v)[4]) {
-    const float* base = dsrc + (a.r0 + tile * 16) * F + lane;
-    if (tile < nfull) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (32 * u < 16 * 7 && lane + 32 * u < 16 * F) ? __ldg(base + 32 * u) : 0.0f;
-    } else {
-      const int64_t left = tile < ntiles ? (a.r1 - a.r0 - tile * 16) * F : 0;  // elements in the tail tile
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (lane + 32 * u < 16 * F && lane + 32 * u < left) ? __ldg(base + 32 * u) : 0.0f;
-    }
-  };
-  auto frag_dense = [&](const float (&v)[4], uint32_t (&a1)[4]) {
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (lane + 32 * u < 16 * F) xw[lane + 32 * u] = v[u];
-    __syncwarp();
-    a1[0] = k0ok ? __float_as_uint(xw[g * F + q]) : c0v;
-    a1[1] = k0ok ? __float_as_uint(xw[(g + 8) * F + q]) : c0v;
-    a1[2] = k1ok ? __float_as_uint(xw[g * F + q + 4]) : c1v;
-    a1[3] = k1ok ? __float_as_uint(xw[(g + 8) * F + q + 4]) : c1v;
-  };
   auto load = [&](int64_t tile, uint32_t (&a1)[4]) {
     const int64_t ra = a.r0 + tile * 16 + g, rb = ra + 8;
     const bool va = tile < ntiles && ra < a.r1, vb = tile < ntiles && rb < a.r1;
     const float* pa = a.src + (va ? in_off(ra) : 0);
     const float* pb = a.src + (vb ? in_off(rb) : 0);
     // layer 1 (tf32, K = 8): a0 = (row g, k = q), a1 = (row g+8, q), a2/a3 = k + 4
-    a1[0] = va && k0ok ? __float_as_uint(__ldg(pa + c0)) : c0v;
-    a1[1] = vb && k0ok ? __float_as_uint(__ldg(pb + c0)) : c0v;
-    a1[2] = va && k1ok ? __float_as_uint(__ldg(pa + c1)) : c1v;
-    a1[3] = vb && k1ok ? __float_as_uint(__ldg(pb + c1)) : c1v;
+    a1[0] = va && k0ok ? __float_as_uint(__ldg(pa + c0)) : 0u;
+    a1[1] = vb && k0ok ? __float_as_uint(__ldg(pb + c0)) : 0u;
+    a1[2] = va && k1ok ? __float_as_uint(__ldg(pa + c1)) : 0u;
+    a1[3] = vb && k1ok ? __float_as_uint(__ldg(pb + c1)) : 0u;
   };
-  uint32_t nxt[4];
-  float nxv[4];
-  if constexpr (DENSE) load_dense(wid, nxv);
-  else load(wid, nxt);
-  for (int64_t tile = wid; tile < ntiles; tile += nw) {
-    uint32_t a1[4];
-    if constexpr (DENSE) {
-      frag_dense(nxv, a1);
-      load_dense(tile + nw, nxv);
-    } else {
-      a1[0] = nxt[0], a1[1] = nxt[1], a1[2] = nxt[2], a1[3] = nxt[3];
-      load(tile + nw, nxt);
-    }
+  // one 16-row tile: forward pass on the MMAs, outputs to the out-plan
+  auto tile_body = [&](const uint32_t (&a1)[4], int64_t tile) {
     float d1[T1][4];
 #pragma unroll
-    for (int t = 0; t < T1; ++t) {
-      d1[t][0] = d1[t][1] = d1[t][2] = d1[t][3] = 0.0f;
-      mma_tf32(d1[t], a1, w1[t][0], w1[t][1]);
-    }
-    // layer 2 (bf16): k16 step k = n8 tiles 2k, 2k + 1 of layer 1; last = bias
+    for (int t = 0; t < T1; ++t) mma_tf32(d1[t], a1, w1[t][0], w1[t][1], sf.b1[t][lane]);
+    // layer 2 (bf16): k16 step k = n8 tiles 2k, 2k + 1 of layer 1
     float d2[T2][4];
 #pragma unroll
-    for (int t = 0; t < T2; ++t) {
-      d2[t][0] = d2[t][1] = d2[t][2] = d2[t][3] = 0.0f;
-      mma_bf16(d2[t], abias, SMM_W2(t, K2 - 1, 0), SMM_W2(t, K2 - 1, 1));
-    }
-#pragma unroll
-    for (int k = 0; k < K2 - 1; ++k) {
+    for (int k = 0; k < K2; ++k) {
       const uint32_t af[4] = {act_pack<ACT1>(d1[2 * k][0], d1[2 * k][1]), act_pack<ACT1>(d1[2 * k][2], d1[2 * k][3]),
                               act_pack<ACT1>(d1[2 * k + 1][0], d1[2 * k + 1][1]),
                               act_pack<ACT1>(d1[2 * k + 1][2], d1[2 * k + 1][3])};
 #pragma unroll
-      for (int t = 0; t < T2; ++t) mma_bf16(d2[t], af, SMM_W2(t, k, 0), SMM_W2(t, k, 1));
+      for (int t = 0; t < T2; ++t) {
+        if (k == 0) mma_bf16_c(d2[t], af, SMM_W2(t, 0, 0), SMM_W2(t, 0, 1), sf.b2[t][lane]);
+        else mma_bf16(d2[t], af, SMM_W2(t, k, 0), SMM_W2(t, k, 1));
+      }
     }
     // layer 3 (bf16, N = 8 holds the outputs)
-    float y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    mma_bf16(y, abias, w3[K3 - 1][0], w3[K3 - 1][1]);
+    float y[4];
 #pragma unroll
-    for (int k = 0; k < K3 - 1; ++k) {
+    for (int k = 0; k < K3; ++k) {
       const uint32_t af[4] = {act_pack<ACT2>(d2[2 * k][0], d2[2 * k][1]), act_pack<ACT2>(d2[2 * k][2], d2[2 * k][3]),
                               act_pack<ACT2>(d2[2 * k + 1][0], d2[2 * k + 1][1]),
                               act_pack<ACT2>(d2[2 * k + 1][2], d2[2 * k + 1][3])};
-      mma_bf16(y, af, w3[k][0], w3[k][1]);
+      if (k == 0) mma_bf16_c(y, af, w3[0][0], w3[0][1], sf.b3[lane]);
+      else mma_bf16(y, af, w3[k][0], w3[k][1]);
     }
     if (a.act3 != SMLRT_IDENTITY) {
 #pragma unroll
@@ -247,6 +249,58 @@ __global__ void __launch_bounds__(128) small_mma_kernel(const __grid_constant__ 
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) chk = fmaf(y[e], 0.0f, chk);
+  };
+
+  int64_t t0 = 0;  // first tile of the per-lane path
+  if constexpr (DENSE) {
+    const int64_t nch = (a.r1 - a.r0) / SMM_CH;
+    const int64_t mine = nch > (int64_t)blockIdx.x ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int sb = smm_stage_floats(F);
+    // chunk c's rows start at gsrc + c * SMM_CH * F; a chunk is a multiple of
+    // 16 B, so every chunk has the same misalignment `al` (floats) and copies
+    // from the 16-B boundary below to the one above -- both inside the
+    // 16-B granules of the array's own first and last bytes
+    const float* gsrc = a.src + P.col_inl[0] + a.r0 * F;
+    const int al = (int)((reinterpret_cast<uintptr_t>(gsrc) & 15) >> 2);
+    const uint32_t bytes = (uint32_t)(((SMM_CH * F + al) * 4 + 15) & ~15);
+    auto issue = [&](int64_t k) {
+      const int s = (int)(k % SMM_S);
+      const float* src = gsrc + (blockIdx.x + k * gridDim.x) * (int64_t)SMM_CH * F - al;
+      expect_tx(&full[s], bytes);
+      bulk_g2s(smem_u32(ring + s * sb), src, bytes, &full[s]);
+    };
+    if (threadIdx.x == 0)
+      for (int64_t k = 0; k < SMM_S && k < mine; ++k) issue(k);
+    for (int64_t k = 0; k < mine; ++k) {
+      const int s = (int)(k % SMM_S);
+      smm_wait(&full[s], (uint32_t)((k / SMM_S) & 1));
+      const float* xs = ring + s * sb + al + warp * (SMM_TPW * 16) * F;
+      uint32_t af[SMM_TPW][4];
+#pragma unroll
+      for (int j = 0; j < SMM_TPW; ++j) {
+        const float* xa = xs + (j * 16 + g) * F;
+        af[j][0] = k0ok ? __float_as_uint(xa[q]) : 0u;
+        af[j][1] = k0ok ? __float_as_uint(xa[8 * F + q]) : 0u;
+        af[j][2] = k1ok ? __float_as_uint(xa[q + 4]) : 0u;
+        af[j][3] = k1ok ? __float_as_uint(xa[8 * F + q + 4]) : 0u;
+      }
+      __syncthreads();  // every warp has its fragments: the stage is free
+      if (threadIdx.x == 0 && k + SMM_S < mine) {
+        fence_async_smem();
+        issue(k + SMM_S);
+      }
+      const int64_t tile0 = (blockIdx.x + k * gridDim.x) * (SMM_CH / 16) + warp * SMM_TPW;
+#pragma unroll
+      for (int j = 0; j < SMM_TPW; ++j) tile_body(af[j], tile0 + j);
+    }
+    t0 = nch * (SMM_CH / 16);
+  }
+  uint32_t nxt[4];
+  load(t0 + wid, nxt);
+  for (int64_t tile = t0 + wid; tile < ntiles; tile += nw) {
+    const uint32_t a1[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+    load(tile + nw, nxt);
+    tile_body(a1, tile);
   }
   if (__any_sync(0xffffffffu, chk != chk) && lane == 0) atomicOr(a.status, SMLRT_STATUS_NONFINITE);
 }
@@ -280,31 +334,33 @@ int build_smm(smlrt_model_s& m) {
   auto w1 = [&](int n, int k) { return n < H1 && k < F ? W1[(size_t)n * F + k] : 0.0f; };
   auto w2 = [&](int n, int k) { return n < H2 && k < H1 ? W2[(size_t)n * H1 + k] : 0.0f; };
   auto w3 = [&](int n, int k) { return n < G && k < H2 ? W3[(size_t)n * H2 + k] : 0.0f; };
-  // layer 1's column F carries b1; layers 2/3 have a bias k step
-  auto w1b = [&](int n, int k) { return k == F ? (n < H1 ? b1[n] : 0.0f) : w1(n, k); };
+  auto bias = [&](const float* b, int n, int nmax) { return n < nmax ? b[n] : 0.0f; };
+  // the C quad of columns (n, n + 1) for rows g and g + 8
+  auto quad = [&](const float* b, int n, int nmax) {
+    return float4{bias(b, n, nmax), bias(b, n + 1, nmax), bias(b, n, nmax), bias(b, n + 1, nmax)};
+  };
   for (int l = 0; l < 32; ++l) {
     const int gg = l >> 2, qq = l & 3;
     for (int t = 0; t < Fr::T1; ++t) {
-      h.w1[t][l][0] = smm_tf32(w1b(8 * t + gg, qq));
-      h.w1[t][l][1] = smm_tf32(w1b(8 * t + gg, qq + 4));
+      h.w1[t][l][0] = smm_tf32(w1(8 * t + gg, qq));
+      h.w1[t][l][1] = smm_tf32(w1(8 * t + gg, qq + 4));
+      h.b1[t][l] = quad(b1, 8 * t + 2 * qq, H1);
     }
     for (int t = 0; t < Fr::T2; ++t) {
       const int n = 8 * t + gg;
-      for (int k = 0; k < Fr::K2 - 1; ++k) {
+      for (int k = 0; k < Fr::K2; ++k) {
         const int kk = 16 * k + 2 * qq;
         h.w2[t][k][l][0] = smm_bf16(w2(n, kk)) | (smm_bf16(w2(n, kk + 1)) << 16);
         h.w2[t][k][l][1] = smm_bf16(w2(n, kk + 8)) | (smm_bf16(w2(n, kk + 9)) << 16);
       }
-      h.w2[t][Fr::K2 - 1][l][0] = qq == 0 && n < H2 ? smm_bf16(b2[n]) : 0u;  // k = 0 of the bias step
-      h.w2[t][Fr::K2 - 1][l][1] = 0u;
+      h.b2[t][l] = quad(b2, 8 * t + 2 * qq, H2);
     }
-    for (int k = 0; k < Fr::K3 - 1; ++k) {
+    for (int k = 0; k < Fr::K3; ++k) {
       const int kk = 16 * k + 2 * qq;
       h.w3[k][l][0] = smm_bf16(w3(gg, kk)) | (smm_bf16(w3(gg, kk + 1)) << 16);
       h.w3[k][l][1] = smm_bf16(w3(gg, kk + 8)) | (smm_bf16(w3(gg, kk + 9)) << 16);
     }
-    h.w3[Fr::K3 - 1][l][0] = qq == 0 && gg < G ? smm_bf16(b3[gg]) : 0u;
-    h.w3[Fr::K3 - 1][l][1] = 0u;
+    h.b3[l] = quad(b3, 2 * qq, G);
   }
   SMLRT_CUDA(cudaMalloc(&m.smm_blob, sizeof(Fr)));
   SMLRT_CUDA(cudaMemcpy(m.smm_blob, &h, sizeof(Fr), cudaMemcpyHostToDevice));
@@ -317,7 +373,7 @@ bool smm_shape(const smlrt_model_s& m, int* n1, int* n2) {
   for (int l = 0; l < 3; ++l)
     if (m.layers[l].kind != SMLRT_DENSE) return false;
   const int F = m.layers[0].in, H1 = m.layers[0].out, H2 = m.layers[1].out, G = m.layers[2].out;
-  if (F > 7 || H1 > 64 || H2 > 64 || G > SMM_G) return false;  // column F carries b1
+  if (F > SMM_F || H1 > 64 || H2 > 64 || G > SMM_G) return false;
   const int a1 = m.layers[0].act, a2 = m.layers[1].act;
   if (a1 != a2) return false;
   auto r16 = [](int n) { return n <= 16 ? 16 : n <= 32 ? 32 : 64; };
@@ -345,21 +401,35 @@ int launch_smm(const smlrt_model_s& m, const DevPlan& in, const void* src, const
   a.act1 = L1.act;
   a.act2 = L2.act;
   a.act3 = L3.act;
-  // persistent grid: one wave of resident CTAs, each warp striding over tiles
+  // persistent grid: one wave of resident CTAs, each warp striding over
+  // tiles (dense rows: over ring chunks); occupancy per feature count, as
+  // the ring's stage size depends on it
   const int64_t tiles = (r1 - r0 + 15) / 16;
-  static int slots = 0;
-  if (!slots) {
+  const int F = in.n_cols;
+  const bool dense = in.n_sweep == 1 && out.n_sweep == 1 && in.dense_rows && in.ustride[0] == in.n_cols;
+  const size_t ring = dense ? (size_t)SMM_S * smm_stage_floats(F) * sizeof(float) : 0;
+  static int slots[2][SMM_F + 1] = {};
+  int& sl = slots[dense][F];
+  if (!sl) {
+    if (dense)  // the ring of 8-feature rows exceeds the 48 KB default
+      SMLRT_CUDA(cudaFuncSetAttribute(small_mma_kernel<N1, N2, ACT1, ACT2, true, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMM_S * smm_stage_floats(SMM_F) * (int)sizeof(float)));
     int dev_id = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id);
-    SMLRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_mma_kernel<N1, N2, ACT1, ACT2, true, false>, 128, 0));
-    slots = std::max(1, per_sm) * sms;
+    if (dense)
+      SMLRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_mma_kernel<N1, N2, ACT1, ACT2, true, true>,
+                                                               128, ring));
+    else
+      SMLRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, small_mma_kernel<N1, N2, ACT1, ACT2, true, false>, 128, 0));
+    sl = std::max(1, per_sm) * sms;
   }
-  const int64_t blocks = std::min<int64_t>((tiles + 3) / 4, slots);
+  const int64_t blocks = std::min<int64_t>((tiles + 3) / 4, sl);
   const unsigned grid = (unsigned)std::max<int64_t>(1, blocks);
-  const bool dense = in.n_sweep == 1 && in.dense_rows && in.ustride[0] == in.n_cols;
-  if (in.n_sweep == 1 && out.n_sweep == 1 && dense)
-    small_mma_kernel<N1, N2, ACT1, ACT2, true, true><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
+  if (dense)
+    small_mma_kernel<N1, N2, ACT1, ACT2, true, true><<<grid, 128, ring, s>>>(a, in, out, static_cast<const Fr*>(dev));
   else if (in.n_sweep == 1 && out.n_sweep == 1)
     small_mma_kernel<N1, N2, ACT1, ACT2, true, false><<<grid, 128, 0, s>>>(a, in, out, static_cast<const Fr*>(dev));
   else

@@ -253,7 +253,8 @@ def _small_chunks(rt):
 
 
 @pytest.mark.parametrize("config,n,shard", [("bonds", 312345, None), ("bonds", 312345, (1, 3)),
-                                            ("options", 312345, None), ("minibude", 312345, None),
+                                            ("options", 312345, None), ("options_bf16", 312345, None),
+                                            ("options_bf16", 312345, (2, 3)), ("minibude", 312345, None),
                                             ("minibude", 312345, (0, 2)), ("particlefilter", 601, None),
                                             ("miniweather", 130 * 300, None), ("miniweather_bf16", 130 * 300, None),
                                             ("miniweather", 130 * 300, (1, 3))])

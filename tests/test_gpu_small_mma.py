@@ -37,13 +37,12 @@ def _act(h, a):
 
 def _emulate(layers, x):
     """the kernel's quantisation points: tf32 features (truncated by the MMA)
-    and tf32 W1 | b1 (b1 rides as the weights of a constant-1 input), bf16
-    hidden activations, bf16 W2 | b2 and W3 | b3 (the biases are an extra
-    k step of the bf16 MMAs), f32 accumulation"""
+    and tf32 W1, bf16 hidden activations, bf16 W2 and W3, f32 biases (each
+    is its accumulator's initial value), f32 accumulation"""
     (w1, b1, a1), (w2, b2, a2), (w3, b3, a3) = layers
-    h = _act(_tf32_trunc(x) @ _tf32_rne(w1).T + _tf32_rne(b1), a1)
-    h = _act(_bf16(h) @ _bf16(w2).T + _bf16(b2), a2)
-    return _act(_bf16(h) @ _bf16(w3).T + _bf16(b3), a3)
+    h = _act(_tf32_trunc(x) @ _tf32_rne(w1).T + b1, a1)
+    h = _act(_bf16(h) @ _bf16(w2).T + b2, a2)
+    return _act(_bf16(h) @ _bf16(w3).T + b3, a3)
 
 
 def _region(dims, n, act, seed=3):
@@ -87,6 +86,7 @@ def _check(wl, got, emulate=True):
 
 
 @pytest.mark.parametrize("dims,act,n", [([5, 64, 32, 1], "relu", 100_003), ([7, 16, 16, 8], "relu", 4097),
+                                        ([8, 16, 16, 8], "relu", 3000), ([8, 64, 64, 8], "tanh", 70_001),
                                         ([3, 40, 24, 3], "relu", 999), ([7, 64, 64, 2], "tanh", 2000),
                                         ([2, 9, 17, 5], "identity", 77), ([5, 64, 32, 1], "relu", 1)])
 @pytest.mark.parametrize("commit", ["fused", "checked"])
@@ -120,9 +120,9 @@ def test_small_mma_nonfinite(cuda, tmp_path, commit):
         assert (wl.buffers["price"].to_numpy() == 3.0).all()
 
 
-def test_eight_features_use_the_chain(cuda, tmp_path):
-    """F = 8 leaves no input column for layer 1's bias: the layer chain runs it."""
-    wl = _region([8, 16, 16, 8], 3000, "relu")
+def test_nine_features_use_the_chain(cuda, tmp_path):
+    """F = 9 does not fit layer 1's k8 MMA: the layer chain runs it."""
+    wl = _region([9, 16, 16, 8], 3000, "relu")
     got, launches = _run(wl, tmp_path)
     assert launches == 5
     ref, _ = c_oracle.mlp_f32(wl.layers, wl.arrays["recs"])
@@ -151,3 +151,20 @@ def test_f64_arrays_take_the_chain(cuda, tmp_path):
     assert launches == 5 and got.dtype == np.float64
     ref, _ = c_oracle.mlp_f32(wl.layers, wl.arrays["recs"].astype(np.float32))
     assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("world", [3, 7])
+def test_small_mma_shards_match_the_whole_call(cuda, tmp_path, world):
+    """Sweep shards start at arbitrary rows, so the packed input rows of a
+    shard start at any 4-B offset of a 16-B bulk-copy granule: every shard's
+    rows are bitwise those of the unsharded call (ring chunks + per-lane
+    tail)."""
+    wl = _region([5, 64, 32, 1], 200_003, "relu")
+    whole, _ = _run(wl, tmp_path)
+    got = np.full_like(whole, np.nan)
+    for r in range(world):
+        wl.arrays["price"][:] = np.nan
+        part, _ = _run(wl, tmp_path, shard=(r, world))
+        done = ~np.isnan(part)
+        got[done] = part[done]
+    assert np.array_equal(got, whole)

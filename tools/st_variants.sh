@@ -10,4 +10,4 @@ build_var() {
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v "$@" -c $src -o build_var/$name/${src%.cu}.o 2> build_var/$name/ptxas.txt || (cat build_var/$name/ptxas.txt; false)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libsmlrt_var_$name.so build_var/$name/*.o -lcudart
 }
-build_var pt256 cnn_exact.cu -DSMLRT_PF_PT=256
+if [ $# -gt 0 ]; then "$@"; fi
