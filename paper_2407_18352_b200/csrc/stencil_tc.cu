@@ -93,9 +93,14 @@ struct SmArgs {
   float b2[SM_G];
 };
 
+#ifdef SM_MMA_VOLATILE
+#define SM_MMA_ASM asm volatile
+#else
+#define SM_MMA_ASM asm
+#endif
 __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
                                           const float (&c)[4]) {
-  asm volatile(
+  SM_MMA_ASM(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%10,%11,%12,%13};"
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
@@ -143,7 +148,7 @@ __host__ __device__ constexpr int sm_kpos(int v, int di, int dj) {
 
 __device__ __forceinline__ void mma_1688_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
                                               const float (&c)[4]) {
-  asm volatile(
+  SM_MMA_ASM(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%10,%11,%12,%13};"
       : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
