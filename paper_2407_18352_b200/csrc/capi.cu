@@ -70,6 +70,7 @@ smlrt_model_s::~smlrt_model_s() {
   cudaFree(tc_blob);
   cudaFree(chain_blob);
   cudaFree(smm_blob);
+  cudaFree(stc_blob);
   cudaSetDevice(prev);
 }
 

@@ -193,6 +193,9 @@ struct smlrt_model_s {
   int chain_first = -1;  // model layer the chain starts at (CNN: the first dense layer)
   // small-MLP warp-MMA kernel (small_mma.cu): per-lane B fragments + biases
   void* smm_blob = nullptr;
+  // small-MLP tcgen05 kernel (small_tc.cu): swizzled tf32 W1 / bf16 W2 images
+  void* stc_blob = nullptr;
+  std::vector<float> stc_epi;  // [b2 | w3 (bf16-rounded) | b3] for the kernel parameters
   ~smlrt_model_s();
 };
 
@@ -238,6 +241,9 @@ int launch_region_wide(const smlrt_model_s& m, const DevPlan& in, const void* co
                        int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 // bf16 halo-stencil regions on tcgen05 (stencil_tc.cu); SMLRT_E_UNSUPPORTED if not that shape
 int small_mma_pack(smlrt_model_s& m);
+int small_tc_pack(smlrt_model_s& m, int n1, int n2);
+int launch_region_small_tc(const smlrt_model_s& m, const DevPlan& in, const void* src, const DevPlan& out, void* dst,
+                           int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);
 int launch_region_small_mma(const smlrt_model_s& m, const DevPlan& in, const void* const* in_ptrs,
                             const int32_t* in_dt, const DevPlan& out, void* const* out_ptrs, const int32_t* out_dt,
                             int64_t r0, int64_t r1, float* staged, cudaStream_t s, uint32_t* status);

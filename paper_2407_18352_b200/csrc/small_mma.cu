@@ -469,6 +469,10 @@ int launch_region_small_mma(const smlrt_model_s& m, const DevPlan& in, const voi
   if (r1 <= r0) return SMLRT_OK;
   const void* src = in_ptrs[in.uarray];
   void* dst = out_ptrs[out.uarray];
+  // 1-D sweeps: the tcgen05 kernel (small_tc.cu); other sweeps and
+  // SMLRT_SMALL_TC=0 take the warp-MMA kernel below
+  const int rc = launch_region_small_tc(m, in, src, out, dst, r0, r1, staged, s, status);
+  if (rc != SMLRT_E_UNSUPPORTED) return rc;
 #define SMM_GO(A, B)                                                                      \
   if (n1 == A && n2 == B) return launch_smm_act<A, B>(m, in, src, out, dst, r0, r1, staged, s, status)
   SMM_GO(64, 32);
@@ -488,6 +492,7 @@ int launch_region_small_mma(const smlrt_model_s& m, const DevPlan& in, const voi
 int small_mma_pack(smlrt_model_s& m) {
   int n1 = 0, n2 = 0;
   if (!smm_shape(m, &n1, &n2)) return SMLRT_OK;
+  if (int rc = small_tc_pack(m, n1, n2)) return rc;
 #define SMM_B(A, B) \
   if (n1 == A && n2 == B) return build_smm<A, B>(m)
   SMM_B(64, 32);

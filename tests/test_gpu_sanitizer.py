@@ -29,6 +29,10 @@ def test_sanitizer_clean(cuda, tool):
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
     out = r.stdout + r.stderr
     tail = out[-4000:]
+    if "smoke ok" not in r.stdout and "closed on this pool" in out:
+        # the GPU pool's wrapper refuses compute-sanitizer (runs under it have
+        # left GPUs needing a reset): nothing was checked
+        pytest.skip("compute-sanitizer refused by the GPU pool: " + out.strip().splitlines()[0][:200])
     assert "smoke ok: smlrt_b200" in r.stdout, tail
     if tool == "memcheck":
         assert r.returncode == 0 and "ERROR SUMMARY: 0 errors" in out, tail

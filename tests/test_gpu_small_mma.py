@@ -1,7 +1,10 @@
 """Small dense MLPs at bf16 on the warp-MMA region kernel (small_mma.cu): C1
 options at precision "bf16" and other 3-layer shapes F <= 8 -> H1, H2 <= 64
 -> G <= 8 -- layer 1 on tf32 MMAs from the gathered f32 features, layers 2-3
-on bf16 MMAs with the activations in registers.  Against the fp32 oracle at
+on bf16 MMAs with the activations in registers -- and, for packed rows with
+F <= 6, the tcgen05 small-MLP kernel (small_tc.cu: layer 1 kind::tf32 with
+the bias as two K columns, layer 2 kind::f16 with its A operand in TMEM,
+layer 3 on the FP32 pipe) at the same quantisation points.  Against the fp32 oracle at
 the bf16 tolerance of SURVEY.md 8(d) (max-abs <= 2e-2 max|ref|, RMSE/RMS <=
 1e-2) and against an emulation of its quantisation points."""
 
@@ -88,7 +91,9 @@ def _check(wl, got, emulate=True):
 @pytest.mark.parametrize("dims,act,n", [([5, 64, 32, 1], "relu", 100_003), ([7, 16, 16, 8], "relu", 4097),
                                         ([8, 16, 16, 8], "relu", 3000), ([8, 64, 64, 8], "tanh", 70_001),
                                         ([3, 40, 24, 3], "relu", 999), ([7, 64, 64, 2], "tanh", 2000),
-                                        ([2, 9, 17, 5], "identity", 77), ([5, 64, 32, 1], "relu", 1)])
+                                        ([2, 9, 17, 5], "identity", 77), ([5, 64, 32, 1], "relu", 1),
+                                        ([6, 64, 64, 8], "tanh", 50_001), ([4, 32, 16, 2], "identity", 3333),
+                                        ([1, 16, 64, 4], "relu", 129)])
 @pytest.mark.parametrize("commit", ["fused", "checked"])
 def test_small_mma_matches_oracle(cuda, tmp_path, dims, act, n, commit):
     wl = _region(dims, n, act)
@@ -168,3 +173,20 @@ def test_small_mma_shards_match_the_whole_call(cuda, tmp_path, world):
         done = ~np.isnan(part)
         got[done] = part[done]
     assert np.array_equal(got, whole)
+
+
+def test_warp_mma_kernel_when_tcgen05_kernel_is_off(cuda):
+    """Packed rows with F <= 6 take the tcgen05 small-MLP kernel
+    (small_tc.cu); SMLRT_SMALL_TC=0 (read once per process) routes them to
+    the warp-MMA kernel, which must meet the same checks: the C1 cases of
+    this file re-run in a subprocess with the switch off."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("SMLRT_SMALL_TC") == "0":
+        pytest.skip("already the warp-MMA run")
+    env = dict(os.environ, SMLRT_SMALL_TC="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
+                        "matches_oracle or options_bf16_config or shards or nonfinite"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
