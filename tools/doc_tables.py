@@ -21,7 +21,7 @@ def par(k):
 
 ROWS = [  # (label, config, kernels, bound text, parity sample)
     ("C1 options 1M, 5-64-32-1 fp32", "options", "`region_exact_kernel`", "of FP32", "all 1M rows"),
-    ("C1 at bf16 (`options_bf16`)", "options_bf16", "`small_mma_kernel<64,32>` (warp MMAs)", "of HBM", "all 1M rows"),
+    ("C1 at bf16 (`options_bf16`)", "options_bf16", "`small_tc_kernel<64,32>` (tcgen05, A2 in TMEM)", "of HBM", "all 1M rows"),
     ("C2 bonds 16.8M, 16-256-128-1 bf16", "bonds", "`mlp3_tc_kernel` (tcgen05)", "of bf16 burst", "262k rows"),
     ("**C3 MiniBUDE 67.1M, 6-1024-512-256-1 bf16 (headline)**", "minibude",
      "`w4_fused_kernel<6,2>` (tcgen05, CTA pairs)", "of bf16 sustained, at the 1 kW power cap", "16k rows"),
