@@ -190,3 +190,24 @@ def test_warp_mma_kernel_when_tcgen05_kernel_is_off(cuda):
                         "matches_oracle or options_bf16_config or shards or nonfinite"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("in_soa,out_soa", [(True, False), (False, True), (True, True)])
+def test_small_mlp_column_layouts(cuda, tmp_path, in_soa, out_soa):
+    """Column-per-feature (SoA) arrays: strided input rows take the warp-MMA
+    kernel's per-lane plan loads, packed input rows with SoA outputs take the
+    tcgen05 kernel's generic output plan (row step 1, column offsets o * n);
+    both against the oracle and the quantisation emulation."""
+    dims, n = [5, 64, 32, 2], 20_011
+    wl = _region(dims, n, "relu", seed=7)
+    x = wl.arrays["recs"]
+    fin = "functor(optin: [k, 0:5] = ([0:5, k]))" if in_soa else "functor(optin: [k, 0:5] = ([k, 0:5]))"
+    fout = "functor(optout: [k, 0:2] = ([0, k], [1, k]))" if out_soa else "functor(optout: [k, 0:2] = ([k, 0], [k, 1]))"
+    wl.arrays = {"recs": np.ascontiguousarray(x.T) if in_soa else x,
+                 "price": np.zeros((2, n) if out_soa else (n, 2), np.float32)}
+    wl.spec = type(wl.spec)(**{**wl.spec.__dict__, "in_functor": fin, "out_functor": fout})
+    got, launches = _run(wl, tmp_path)
+    assert launches == 1
+    got = got.T if out_soa else got
+    wl.arrays["recs"] = x  # the checks read row-major features
+    _check(wl, np.ascontiguousarray(got).astype(np.float64))
