@@ -16,9 +16,10 @@
 //     the packed pairs back into the SAME lane's TMEM columns (tcgen05.st):
 //     they are layer 2's A operand (TS form), no shared-memory round trip;
 //   * layer 2: H1/16 kind::f16 TS MMAs M=128 N=H2 into the columns after A2;
-//   * layer 3 (G <= 8 outputs) on the FP32 pipe in the epilogue: act(acc +
-//     b2) rounded to bf16, times bf16 W3, f32 accumulation -- the weights
-//     are compile-time-indexed kernel parameters (constant-bank operands);
+//   * layer 3 (G <= 8 outputs): act(acc2 + b2) as bf16 pairs back into the
+//     lane's TMEM, one more TS MMA chain M=128 N=16 (STC_L3MMA; or packed
+//     f32x2 FMAs on the FP32 pipe with the weights as compile-time-indexed
+//     kernel parameters);
 //   * several CTAs per SM (64 TMEM columns each for 64-32) interleave their
 //     chains; no warp specialisation, no cross-CTA handshakes.
 // Quantisation points are those of the warp-MMA kernel (small_mma.cu), so
@@ -44,6 +45,9 @@ constexpr int STC_G = 8, STC_F = 6, STC_H = 64;  // F <= 6: K = 8 holds the feat
 #ifndef STC_MINB
 #define STC_MINB 8
 #endif
+#ifndef STC_L3MMA
+#define STC_L3MMA 1  // layer 3 as a TS MMA (N = 16) instead of packed FMAs on the FP32 pipe
+#endif
 #ifndef STC_E1
 #define STC_E1 16  // acc1 columns drained per tcgen05.ld wait (16 or 32; 32 needs N1 >= 32)
 #endif
@@ -53,7 +57,7 @@ struct StcArgs {
   const float* src;     // row 0's first feature: packed rows of F floats
   float* obase;  // out-plan array, or the checked commit's staging shifted by -r0 * g
   uint32_t* status;
-  const uint8_t* blob;  // [W1 (K = 8 tf32)][W2 K16-blocks (bf16)], SW32 images
+  const uint8_t* blob;  // [W1 (K = 8 tf32)][W2 K16-blocks][W3 K16-blocks] (bf16), SW32 images
   int64_t op;           // output element step per sweep row
   int64_t ocol[STC_G];  // output column offsets (out-plan, or 0..g-1 staged)
   int F, g, act3;
@@ -101,13 +105,17 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
   constexpr int TC = stc_cols(N1, N2);
   constexpr int W1B = N1 * 32, W2B = N2 * 32, K2 = N1 / 16;
   constexpr int A2C = 0, D2C = N1 / 2;  // TMEM columns: A2 over acc1's drained half, acc2 after it
+  // layer 3 (STC_L3MMA): A3 = the packed bf16 layer-2 activations over the
+  // dead A2 columns [0, N2/2), acc3 (16 columns, G <= 8 used) after A3
+  constexpr int A3C = 0, D3C = N2 / 2, K3 = N2 / 16, W3B = 16 * 32;
+  static_assert(!STC_L3MMA || D3C + 16 <= TC, "acc3 fits the allocation");
   __shared__ __align__(1024) uint8_t sA1[128 * 32];
-  __shared__ __align__(1024) uint8_t sW[W1B + K2 * W2B];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(1024) uint8_t sW[W1B + K2 * W2B + (STC_L3MMA ? K3 * W3B : 0)];
+  __shared__ __align__(8) uint64_t bar[3];
   __shared__ uint32_t slot;
   const int tid = threadIdx.x, warp = tid >> 5;
   {  // weights -> shared memory: every load in flight before the first store
-    constexpr int NV = (W1B + K2 * W2B) / 16, PER = (NV + 127) / 128;
+    constexpr int NV = (W1B + K2 * W2B + (STC_L3MMA ? K3 * W3B : 0)) / 16, PER = (NV + 127) / 128;
     const int4* g = reinterpret_cast<const int4*>(a.blob);
     int4* d = reinterpret_cast<int4*>(sW);
     int4 t[PER];
@@ -121,6 +129,7 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     mbar_fence_init();
   }
   if (warp == 0) tmem_alloc(&slot, TC);
@@ -134,6 +143,8 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
   const uint64_t a1d = smem_desc(a1s, 256, kSwizzle32);
   const uint64_t w1d = smem_desc(ws, 256, kSwizzle32);
   const uint64_t w2d = smem_desc(ws + W1B, 256, kSwizzle32);
+  const uint64_t w3d = smem_desc(ws + W1B + K2 * W2B, 256, kSwizzle32);
+  constexpr uint32_t id3 = idesc_bf16(128, 16);
   constexpr uint32_t id1 = idesc_tf32(128, N1), id2 = idesc_bf16(128, N2);
 
   const int64_t ntiles = (a.r1 - a.r0 + 127) / 128;
@@ -211,11 +222,47 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
     __syncthreads();
     tc_fence_after();
     // ---- layer 2 epilogue + layer 3 on the FP32 pipe
+    const uint64_t* b2p = reinterpret_cast<const uint64_t*>(a.b2);
+    float y[GP];
+#if STC_L3MMA
+    // act(acc2 + b2) as bf16 pairs into this lane's A3 columns, then one
+    // N = 16 TS MMA chain (K = N2) gives the G outputs
+#pragma unroll
+    for (int c = 0; c < N2; c += 16) {
+      uint32_t r[16], h[8];
+      tmem_ld16(my + D2C + c, r);
+      tmem_wait_ld16(r);
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {
+        const uint64_t z = stc_add2(stc_pair(__uint_as_float(r[e]), __uint_as_float(r[e + 1])), b2p[(c + e) / 2]);
+        h[e / 2] = stc_pack<ACT>(__uint_as_float((uint32_t)z), __uint_as_float((uint32_t)(z >> 32)));
+      }
+      tmem_st8(my + A3C + c / 2, h);  // columns below D2C + c: already drained
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < K3; ++k) mma_ts_elect(tb + D3C, tb + A3C + 8 * k, w3d + ((k * W3B) >> 4), id3, k > 0);
+      mma_commit_elect(&bar[2]);
+      mbar_wait_sleep(&bar[2], it & 1);
+    }
+    __syncthreads();
+    tc_fence_after();
+    {
+      uint32_t r[16];
+      tmem_ld16(my + D3C, r);
+      tmem_wait_ld16(r);
+#pragma unroll
+      for (int o = 0; o < GP; ++o) y[o] = __uint_as_float(r[o]) + a.b3[o];
+    }
+#else
     // y = b3 + sum_k bf16(act(acc2_k + b2_k)) * w3_k as even/odd packed partial sums
     uint64_t y2[GP];
 #pragma unroll
     for (int o = 0; o < GP; ++o) y2[o] = 0ull;
-    const uint64_t* b2p = reinterpret_cast<const uint64_t*>(a.b2);
 #pragma unroll
     for (int c = 0; c < N2; c += 16) {
       uint32_t r[16];
@@ -231,10 +278,10 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
           y2[o] = stc_fma2(hh, reinterpret_cast<const uint64_t*>(a.w3[o])[(c + e) / 2], y2[o]);
       }
     }
-    float y[GP];
 #pragma unroll
     for (int o = 0; o < GP; ++o)
       y[o] = (__uint_as_float((uint32_t)y2[o]) + __uint_as_float((uint32_t)(y2[o] >> 32))) + a.b3[o];
+#endif
     if (row < a.r1) {
 #pragma unroll
       for (int o = 0; o < GP; ++o)
@@ -351,7 +398,8 @@ int small_tc_pack(smlrt_model_s& m, int n1, int n2) {
   const float *W1 = p, *b1 = W1 + (size_t)H1 * F, *W2 = b1 + H1, *b2 = W2 + (size_t)H2 * H1, *W3 = b2 + H2,
               *b3 = W3 + (size_t)G * H2;
   const size_t w1b = (size_t)n1 * 32, w2b = (size_t)n2 * 32;
-  std::vector<uint8_t> img(w1b + (size_t)(n1 / 16) * w2b, 0);
+  // [W1][W2 K16-blocks][W3 K16-blocks: 16 rows (outputs, zero past G) x 32 B]
+  std::vector<uint8_t> img(w1b + (size_t)(n1 / 16) * w2b + (size_t)(n2 / 16) * 512, 0);
   for (int n = 0; n < H1; ++n)
     for (int k = 0; k < 8; ++k) {  // features 0..F-1, zeros, the bias as tf32 hi + lo at 6, 7
       float w = 0.0f;
@@ -365,6 +413,11 @@ int small_tc_pack(smlrt_model_s& m, int n1, int n2) {
     for (int k = 0; k < H1; ++k) {
       const uint16_t h = stc_bf16(W2[(size_t)n * H1 + k]);
       std::memcpy(img.data() + w1b + (k / 16) * w2b + sw32_byte(n, (k % 16) * 2), &h, 2);
+    }
+  for (int o = 0; o < G; ++o)
+    for (int k = 0; k < H2; ++k) {
+      const uint16_t h = stc_bf16(W3[(size_t)o * H2 + k]);
+      std::memcpy(img.data() + w1b + (size_t)(n1 / 16) * w2b + (k / 16) * 512 + sw32_byte(o, (k % 16) * 2), &h, 2);
     }
   m.stc_epi.assign(STC_H + STC_G * STC_H + STC_G, 0.0f);
   for (int n = 0; n < H2; ++n) m.stc_epi[n] = b2[n];
