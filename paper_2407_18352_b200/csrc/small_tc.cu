@@ -7,11 +7,12 @@
 // is ~1 us of tensor work split into two tiny MMAs, so the kernel is built
 // around latency, not tensor throughput:
 //   * one CTA = one 128-row chain: thread t owns row t = TMEM lane t.  Its
-//     features go straight from global memory (prefetched one tile ahead in
-//     registers) into a 32-B-per-row SW32 tile of tf32 values; two extra
-//     columns hold 1.0 and the weights tf32(b1) and tf32(b1 - tf32(b1)), so
-//     layer 1's bias rides in the MMA at ~f32 precision;
-//   * layer 1: one (F + 2 <= 8) or two kind::tf32 MMAs M=128 N=H1 -> TMEM;
+//     packed row of F <= 6 features goes straight from global memory
+//     (prefetched one tile ahead in registers) into a 32-B-per-row SW32 tile
+//     of tf32 values; K columns 6 and 7 hold 1.0 and their weights are
+//     tf32(b1) and tf32(b1 - tf32(b1)), so layer 1's bias rides in the MMA
+//     at ~f32 precision;
+//   * layer 1: one kind::tf32 MMA M=128 N=H1 K=8 -> TMEM;
 //   * each thread drains its lane (tcgen05.ld), act + bf16 pack, and stores
 //     the packed pairs back into the SAME lane's TMEM columns (tcgen05.st):
 //     they are layer 2's A operand (TS form), no shared-memory round trip;
