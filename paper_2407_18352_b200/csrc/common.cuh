@@ -193,9 +193,9 @@ struct smlrt_model_s {
   int chain_first = -1;  // model layer the chain starts at (CNN: the first dense layer)
   // small-MLP warp-MMA kernel (small_mma.cu): per-lane B fragments + biases
   void* smm_blob = nullptr;
-  // small-MLP tcgen05 kernel (small_tc.cu): swizzled tf32 W1 / bf16 W2 images
+  // small-MLP tcgen05 kernel (small_tc.cu): swizzled tf32 W1 / bf16 W2, W3 images
   void* stc_blob = nullptr;
-  std::vector<float> stc_epi;  // [b2 | w3 (bf16-rounded) | b3] for the kernel parameters
+  std::vector<float> stc_epi;  // [b2 (64) | b3 (8)] for the kernel parameters
   ~smlrt_model_s();
 };
 

@@ -18,11 +18,11 @@
 //     they are layer 2's A operand (TS form), no shared-memory round trip;
 //   * layer 2: H1/16 kind::f16 TS MMAs M=128 N=H2 into the columns after A2;
 //   * layer 3 (G <= 8 outputs): act(acc2 + b2) as bf16 pairs back into the
-//     lane's TMEM, one more TS MMA chain M=128 N=16 (STC_L3MMA; or packed
-//     f32x2 FMAs on the FP32 pipe with the weights as compile-time-indexed
-//     kernel parameters);
-//   * several CTAs per SM (64 TMEM columns each for 64-32) interleave their
-//     chains; no warp specialisation, no cross-CTA handshakes.
+//     lane's TMEM, one more TS MMA chain M=128 N=16 (measured equal to
+//     packed f32x2 FMAs on the FP32 pipe, with 40 fewer instructions per 32
+//     rows);
+//   * 8 chains per SM (4 for H2 = 64: 64 / 128 TMEM columns each), one per
+//     CTA by default (STC_CPS), interleave with no cross-chain handshakes.
 // Quantisation points are those of the warp-MMA kernel (small_mma.cu), so
 // both are checked against one emulation (tests/test_gpu_small_mma.py).
 #include <cuda_bf16.h>
@@ -43,15 +43,6 @@ namespace {
 using namespace ptx;
 
 constexpr int STC_G = 8, STC_F = 6, STC_H = 64;  // F <= 6: K = 8 holds the features and two bias columns
-#ifndef STC_MINB
-#define STC_MINB 8
-#endif
-#ifndef STC_L3MMA
-#define STC_L3MMA 1  // layer 3 as a TS MMA (N = 16) instead of packed FMAs on the FP32 pipe
-#endif
-#ifndef STC_E1
-#define STC_E1 16  // acc1 columns drained per tcgen05.ld wait (16 or 32; 32 needs N1 >= 32)
-#endif
 
 struct StcArgs {
   int64_t r0, r1;
@@ -63,13 +54,22 @@ struct StcArgs {
   int64_t ocol[STC_G];  // output column offsets (out-plan, or 0..g-1 staged)
   int F, g, act3;
   alignas(8) float b2[STC_H];
-  alignas(8) float w3[STC_G][STC_H];  // bf16-rounded
   float b3[STC_G];
 };
 
 __host__ __device__ constexpr int stc_cols(int n1, int n2) {
   const int need = n1 > n1 / 2 + n2 ? n1 : n1 / 2 + n2;
   return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : 256;
+}
+// 128-row chains per SM (all of TMEM, at most 8) and per CTA (STC_CPS)
+#ifndef STC_CPS
+#define STC_CPS 1  // measured on C1 bf16: 1 / 2 / 4 / 8 chains per CTA = 22.2 / 22.6 / 23.1 / 24.6 us
+#endif
+__host__ __device__ constexpr int stc_sm_chains(int n1, int n2) {
+  return 512 / stc_cols(n1, n2) < 8 ? 512 / stc_cols(n1, n2) : 8;
+}
+__host__ __device__ constexpr int stc_chains(int n1, int n2) {
+  return stc_sm_chains(n1, n2) < STC_CPS ? stc_sm_chains(n1, n2) : STC_CPS;
 }
 
 template <int ACT>
@@ -91,56 +91,39 @@ __device__ __forceinline__ uint64_t stc_add2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-__device__ __forceinline__ uint64_t stc_fma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
 // SW32 K-major: 32-B rows, 16-B chunk c of row r at chunk c ^ ((r >> 2) & 1)
 __device__ __forceinline__ uint32_t sw32_chunk(uint32_t row, uint32_t c) {
   return row * 32u + ((c ^ ((row >> 2) & 1u)) << 4);
 }
 
+__device__ __forceinline__ void stc_chain_sync(int chain) {  // the chain's 4 warps (named barrier 1 + chain)
+  asm volatile("bar.sync %0, 128;" ::"r"(chain + 1) : "memory");
+}
+
+// NCH chains per CTA (STC_CPS), 8 / NCH CTAs per SM.  A kernel that may
+// allocate TMEM gets a new CTA on an SM only after the resident ones have
+// released their allocation permit (tools/tmem_occupancy.cu: 8 x 20-us CTAs
+// per SM holding 64 columns each take 47 us, not 20), so the allocation is
+// the kernel's first instruction; one 8-chain CTA per SM has no launch ramp
+// at all but runs each tile slower (named barriers of one CTA, its MMAs in
+// one issue order): 1 chain per CTA is the fastest on C1 (22.2 vs 24.6 us)
 template <int N1, int N2, int ACT, int GP>
-__global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_constant__ StcArgs a) {
-  constexpr int TC = stc_cols(N1, N2);
+__global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2) / stc_chains(N1, N2)) small_tc_kernel(const __grid_constant__ StcArgs a) {
+  constexpr int TC = stc_cols(N1, N2), NCH = stc_chains(N1, N2);
   constexpr int W1B = N1 * 32, W2B = N2 * 32, K2 = N1 / 16;
   constexpr int A2C = 0, D2C = N1 / 2;  // TMEM columns: A2 over acc1's drained half, acc2 after it
-  // layer 3 (STC_L3MMA): A3 = the packed bf16 layer-2 activations over the
+  // layer 3: A3 = the packed bf16 layer-2 activations over the
   // dead A2 columns [0, N2/2), acc3 (16 columns, G <= 8 used) after A3
   constexpr int A3C = 0, D3C = N2 / 2, K3 = N2 / 16, W3B = 16 * 32;
-  static_assert(!STC_L3MMA || D3C + 16 <= TC, "acc3 fits the allocation");
-  __shared__ __align__(1024) uint8_t sA1[128 * 32];
-  __shared__ __align__(1024) uint8_t sW[W1B + K2 * W2B + (STC_L3MMA ? K3 * W3B : 0)];
-  __shared__ __align__(8) uint64_t bar[3];
+  static_assert(D3C + 16 <= TC, "acc3 fits the allocation");
+  __shared__ __align__(1024) uint8_t sA1[NCH][128 * 32];
+  __shared__ __align__(1024) uint8_t sW[W1B + K2 * W2B + K3 * W3B];
+  __shared__ __align__(8) uint64_t bar[NCH][3];
   __shared__ uint32_t slot;
   const int tid = threadIdx.x, warp = tid >> 5;
-  {  // weights -> shared memory: every load in flight before the first store
-    constexpr int NV = (W1B + K2 * W2B + (STC_L3MMA ? K3 * W3B : 0)) / 16, PER = (NV + 127) / 128;
-    const int4* g = reinterpret_cast<const int4*>(a.blob);
-    int4* d = reinterpret_cast<int4*>(sW);
-    int4 t[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (tid + 128 * j < NV) t[j] = __ldg(g + tid + 128 * j);
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (tid + 128 * j < NV) d[tid + 128 * j] = t[j];
-  }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
-    mbar_fence_init();
-  }
-  if (warp == 0) tmem_alloc(&slot, TC);
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tb = slot;
-  const uint32_t my = tb + ((uint32_t)(warp * 32) << 16);  // this warp's 32 lanes
-  const uint32_t a1s = smem_u32(sA1), ws = smem_u32(sW);
+  const int ch = warp >> 2, ct = tid & 127, wq = warp & 3;  // chain, row in the tile, TMEM lane quarter
+  if (warp == 0) tmem_alloc(&slot, TC * NCH);  // first: releases the allocation permit early
+  const uint32_t a1s = smem_u32(sA1[ch]), ws = smem_u32(sW);
   const uint64_t a1d = smem_desc(a1s, 256, kSwizzle32);
   const uint64_t w1d = smem_desc(ws, 256, kSwizzle32);
   const uint64_t w2d = smem_desc(ws + W1B, 256, kSwizzle32);
@@ -153,8 +136,9 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
   float chk = 0.0f;  // y * 0 accumulates NaN iff an output is non-finite
   // this thread's row and pointers, advanced by the grid stride per tile;
   // rows past the end re-read the last row (their outputs are not stored)
-  int64_t row = a.r0 + (int64_t)blockIdx.x * 128 + tid;
-  const int64_t step = (int64_t)gridDim.x * 128;
+  const int64_t tile0 = (int64_t)blockIdx.x * NCH + ch, tstep = (int64_t)gridDim.x * NCH;
+  int64_t row = a.r0 + tile0 * 128 + ct;
+  const int64_t step = tstep * 128;
   const float* const plast = a.src + (a.r1 - 1) * F;
   const float* pi = a.src + row * F;
   float* po = a.obase + row * a.op;
@@ -165,69 +149,77 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
 #pragma unroll
     for (int f = 0; f < STC_F; ++f) x[f] = f < F ? __ldg(p + f) : 0.0f;
   };
-  load(pi);
+  load(pi);  // the first tile's features in flight during the prologue below
+  {  // weights -> shared memory (once per SM): every load in flight before the first store
+    constexpr int NV = (W1B + K2 * W2B + K3 * W3B) / 16, NT = 128 * NCH, PER = (NV + NT - 1) / NT;
+    const int4* g = reinterpret_cast<const int4*>(a.blob);
+    int4* d = reinterpret_cast<int4*>(sW);
+    int4 t[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (tid + NT * j < NV) t[j] = __ldg(g + tid + NT * j);
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (tid + NT * j < NV) d[tid + NT * j] = t[j];
+  }
+  if (ct == 0) {
+    mbar_init(&bar[ch][0], 1);
+    mbar_init(&bar[ch][1], 1);
+    mbar_init(&bar[ch][2], 1);
+    mbar_fence_init();
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = slot + ch * TC;                   // this chain's columns
+  const uint32_t my = tb + ((uint32_t)(wq * 32) << 16);  // this warp's 32 lanes of them
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++it) {
     // ---- layer-1 A tile: tf32 features (truncated as the MMA reads them) in
     // K columns 0..F-1, zeros up to 5, 1.0 in the bias columns 6 and 7
     constexpr uint32_t kOne = 0x3F800000u, kT = 0xFFFFE000u;
-    st_shared_v4(a1s + sw32_chunk(tid, 0), __float_as_uint(x[0]) & kT, __float_as_uint(x[1]) & kT,
+    st_shared_v4(a1s + sw32_chunk(ct, 0), __float_as_uint(x[0]) & kT, __float_as_uint(x[1]) & kT,
                  __float_as_uint(x[2]) & kT, __float_as_uint(x[3]) & kT);
-    st_shared_v4(a1s + sw32_chunk(tid, 1), __float_as_uint(x[4]) & kT, __float_as_uint(x[5]) & kT, kOne, kOne);
+    st_shared_v4(a1s + sw32_chunk(ct, 1), __float_as_uint(x[4]) & kT, __float_as_uint(x[5]) & kT, kOne, kOne);
     pi += step * F;
     load(pi);  // next tile's features in flight during this tile's chain
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
+    stc_chain_sync(ch);
+    if (wq == 0) {
       tc_fence_after();
       mma_tf32_ss_elect(tb, a1d, w1d, id1, 0);
-      mma_commit_elect(&bar[0]);
-      mbar_wait_sleep(&bar[0], it & 1);  // the issuing warp waits; the others sleep in the barrier
+      mma_commit_elect(&bar[ch][0]);
+      mbar_wait_sleep(&bar[ch][0], it & 1);  // the issuing warp waits; the others sleep in the barrier
     }
-    __syncthreads();
+    stc_chain_sync(ch);
     tc_fence_after();
     // ---- layer-1 epilogue: act + bf16 pairs back into this lane's columns (layer 2's A)
 #pragma unroll
-    constexpr int E1 = N1 >= 32 ? STC_E1 : 16;
-    for (int c = 0; c < N1; c += E1) {
-      uint32_t r[E1], p[E1 / 2];
-      if constexpr (E1 == 32) {
-        uint32_t (&r0)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
-        uint32_t (&r1)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[16]);
-        tmem_ld16(my + c, r0);
-        tmem_ld16(my + c + 16, r1);
-        tmem_wait_ld16(r0);
-        tmem_wait_ld16(r1);
-      } else {
-        tmem_ld16(my + c, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-        tmem_wait_ld16(*reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-      }
+    for (int c = 0; c < N1; c += 16) {
+      uint32_t r[16], p[8];
+      tmem_ld16(my + c, r);
+      tmem_wait_ld16(r);
 #pragma unroll
-      for (int e = 0; e < E1 / 2; ++e)
-        p[e] = stc_pack<ACT>(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-      // columns [c/2, c/2 + E1/2) of acc1 were drained by this or an earlier chunk
-#pragma unroll
-      for (int h = 0; h < E1 / 16; ++h) tmem_st8(my + A2C + c / 2 + 8 * h, *reinterpret_cast<uint32_t(*)[8]>(&p[8 * h]));
+      for (int e = 0; e < 8; ++e) p[e] = stc_pack<ACT>(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+      tmem_st8(my + A2C + c / 2, p);  // columns [c/2, c/2 + 8) of acc1 were drained by this or an earlier chunk
     }
     tmem_wait_st();
     tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
+    stc_chain_sync(ch);
+    if (wq == 0) {
       tc_fence_after();
 #pragma unroll
       for (int k = 0; k < K2; ++k) mma_ts_elect(tb + D2C, tb + A2C + 8 * k, w2d + ((k * W2B) >> 4), id2, k > 0);
-      mma_commit_elect(&bar[1]);
-      mbar_wait_sleep(&bar[1], it & 1);
+      mma_commit_elect(&bar[ch][1]);
+      mbar_wait_sleep(&bar[ch][1], it & 1);
     }
-    __syncthreads();
+    stc_chain_sync(ch);
     tc_fence_after();
-    // ---- layer 2 epilogue + layer 3 on the FP32 pipe
+    // ---- layer-2 epilogue: act(acc2 + b2) as bf16 pairs into this lane's
+    // A3 columns, then one N = 16 TS MMA chain (K = N2) gives the G outputs
     const uint64_t* b2p = reinterpret_cast<const uint64_t*>(a.b2);
-    float y[GP];
-#if STC_L3MMA
-    // act(acc2 + b2) as bf16 pairs into this lane's A3 columns, then one
-    // N = 16 TS MMA chain (K = N2) gives the G outputs
 #pragma unroll
     for (int c = 0; c < N2; c += 16) {
       uint32_t r[16], h[8];
@@ -242,16 +234,17 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
     }
     tmem_wait_st();
     tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
+    stc_chain_sync(ch);
+    if (wq == 0) {
       tc_fence_after();
 #pragma unroll
       for (int k = 0; k < K3; ++k) mma_ts_elect(tb + D3C, tb + A3C + 8 * k, w3d + ((k * W3B) >> 4), id3, k > 0);
-      mma_commit_elect(&bar[2]);
-      mbar_wait_sleep(&bar[2], it & 1);
+      mma_commit_elect(&bar[ch][2]);
+      mbar_wait_sleep(&bar[ch][2], it & 1);
     }
-    __syncthreads();
+    stc_chain_sync(ch);
     tc_fence_after();
+    float y[GP];
     {
       uint32_t r[16];
       tmem_ld16(my + D3C, r);
@@ -259,30 +252,6 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
 #pragma unroll
       for (int o = 0; o < GP; ++o) y[o] = __uint_as_float(r[o]) + a.b3[o];
     }
-#else
-    // y = b3 + sum_k bf16(act(acc2_k + b2_k)) * w3_k as even/odd packed partial sums
-    uint64_t y2[GP];
-#pragma unroll
-    for (int o = 0; o < GP; ++o) y2[o] = 0ull;
-#pragma unroll
-    for (int c = 0; c < N2; c += 16) {
-      uint32_t r[16];
-      tmem_ld16(my + D2C + c, r);
-      tmem_wait_ld16(r);
-#pragma unroll
-      for (int e = 0; e < 16; e += 2) {
-        const uint64_t z = stc_add2(stc_pair(__uint_as_float(r[e]), __uint_as_float(r[e + 1])), b2p[(c + e) / 2]);
-        const uint32_t h = stc_pack<ACT>(__uint_as_float((uint32_t)z), __uint_as_float((uint32_t)(z >> 32)));
-        const uint64_t hh = stc_pair(__uint_as_float(h << 16), __uint_as_float(h & 0xFFFF0000u));
-#pragma unroll
-        for (int o = 0; o < GP; ++o)
-          y2[o] = stc_fma2(hh, reinterpret_cast<const uint64_t*>(a.w3[o])[(c + e) / 2], y2[o]);
-      }
-    }
-#pragma unroll
-    for (int o = 0; o < GP; ++o)
-      y[o] = (__uint_as_float((uint32_t)y2[o]) + __uint_as_float((uint32_t)(y2[o] >> 32))) + a.b3[o];
-#endif
     if (row < a.r1) {
 #pragma unroll
       for (int o = 0; o < GP; ++o)
@@ -300,7 +269,7 @@ __global__ void __launch_bounds__(128, STC_MINB) small_tc_kernel(const __grid_co
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tb, TC);
+    tmem_dealloc(slot, TC * NCH);
   }
 }
 
@@ -330,30 +299,17 @@ uint32_t sw32_byte(uint32_t row, uint32_t byte) {
 
 template <int N1, int N2, int ACT, int GP>
 int launch_act(const StcArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
-  constexpr int TC = stc_cols(N1, N2);
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 148;
+  constexpr int NCH = stc_chains(N1, N2), CPS = stc_sm_chains(N1, N2) / NCH;  // CTAs per SM
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // resident CTAs: registers and shared memory (cudaFuncGetAttributes), and
-    // TMEM -- CTAs beyond its 512 columns would block in tcgen05.alloc.  (The
-    // occupancy API reports 1 CTA per SM for this kernel; ncu's theoretical
-    // occupancy and the measured sweep agree with the attribute arithmetic.)
-    cudaFuncAttributes fa{};
-    SMLRT_CUDA(cudaFuncGetAttributes(&fa, small_tc_kernel<N1, N2, ACT, GP>));
-    const int by_regs = 65536 / (std::max(1, fa.numRegs) * 128);
-    const int by_smem = (227 * 1024) / (int)(fa.sharedSizeBytes + 1024);
-    int want = std::min(std::min(by_regs, by_smem), std::min(STC_MINB, 512 / TC));
-    if (const char* e = std::getenv("SMLRT_STC_PER_SM")) want = std::min(std::atoi(e), 512 / TC);
-    if (std::getenv("SMLRT_STC_DEBUG"))
-      fprintf(stderr, "small_tc<%d,%d,%d>: %d regs, %zu B smem, %d CTAs per SM, %d SMs\n", N1, N2, GP, fa.numRegs,
-              fa.sharedSizeBytes, want, sms);
-    slots = std::max(1, want) * sms;
   }
+  // one CTA (NCH chains) per SM at most; fewer when the call has fewer tiles
   const int64_t tiles = (r1 - r0 + 127) / 128;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, slots));
-  small_tc_kernel<N1, N2, ACT, GP><<<grid, 128, 0, s>>>(a);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tiles + NCH - 1) / NCH, (int64_t)sms * CPS));
+  small_tc_kernel<N1, N2, ACT, GP><<<grid, 128 * NCH, 0, s>>>(a);
   count_launch();
   SMLRT_CUDA(cudaGetLastError());
   return SMLRT_OK;
@@ -420,11 +376,9 @@ int small_tc_pack(smlrt_model_s& m, int n1, int n2) {
       const uint16_t h = stc_bf16(W3[(size_t)o * H2 + k]);
       std::memcpy(img.data() + w1b + (size_t)(n1 / 16) * w2b + (k / 16) * 512 + sw32_byte(o, (k % 16) * 2), &h, 2);
     }
-  m.stc_epi.assign(STC_H + STC_G * STC_H + STC_G, 0.0f);
+  m.stc_epi.assign(STC_H + STC_G, 0.0f);  // [b2 | b3]
   for (int n = 0; n < H2; ++n) m.stc_epi[n] = b2[n];
-  for (int o = 0; o < G; ++o)
-    for (int k = 0; k < H2; ++k) m.stc_epi[STC_H + o * STC_H + k] = stc_float((uint32_t)stc_bf16(W3[(size_t)o * H2 + k]) << 16);
-  for (int o = 0; o < G; ++o) m.stc_epi[STC_H + STC_G * STC_H + o] = b3[o];
+  for (int o = 0; o < G; ++o) m.stc_epi[STC_H + o] = b3[o];
   SMLRT_CUDA(cudaMalloc(&m.stc_blob, img.size()));
   SMLRT_CUDA(cudaMemcpy(m.stc_blob, img.data(), img.size(), cudaMemcpyHostToDevice));
   return SMLRT_OK;
@@ -461,8 +415,7 @@ int launch_region_small_tc(const smlrt_model_s& m, const DevPlan& in, const void
     for (int o = 0; o < G; ++o) a.ocol[o] = out.col_inl[o];
   }
   std::memcpy(a.b2, m.stc_epi.data(), sizeof(a.b2));
-  std::memcpy(a.w3, m.stc_epi.data() + STC_H, sizeof(a.w3));
-  std::memcpy(a.b3, m.stc_epi.data() + STC_H + STC_G * STC_H, sizeof(a.b3));
+  std::memcpy(a.b3, m.stc_epi.data() + STC_H, sizeof(a.b3));
   const int act = L1.act;
 #define STC_GO(A, B) \
   if (n1 == A && n2 == B) return launch_shape<A, B>(a, act, r0, r1, s)
