@@ -96,8 +96,12 @@ __device__ __forceinline__ uint32_t sw32_chunk(uint32_t row, uint32_t c) {
   return row * 32u + ((c ^ ((row >> 2) & 1u)) << 4);
 }
 
+template <int NCH>
 __device__ __forceinline__ void stc_chain_sync(int chain) {  // the chain's 4 warps (named barrier 1 + chain)
-  asm volatile("bar.sync %0, 128;" ::"r"(chain + 1) : "memory");
+  if constexpr (NCH == 1)
+    __syncthreads();  // a constant barrier id: a runtime one reserves all 16 and caps CTAs per SM
+  else
+    asm volatile("bar.sync %0, 128;" ::"r"(chain + 1) : "memory");
 }
 
 // NCH chains per CTA (STC_CPS), 8 / NCH CTAs per SM.  A kernel that may
@@ -120,7 +124,10 @@ __global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2
   __shared__ __align__(1024) uint8_t sW[W1B + K2 * W2B + K3 * W3B];
   __shared__ __align__(8) uint64_t bar[NCH][3];
   __shared__ uint32_t slot;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  // the warp index through a shuffle from lane 0 is warp-uniform to the
+  // compiler: the TMEM addresses below live in uniform registers (no R2UR
+  // per tcgen05.ld/st) and the issuing-warp branches are uniform
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int ch = warp >> 2, ct = tid & 127, wq = warp & 3;  // chain, row in the tile, TMEM lane quarter
   if (warp == 0) tmem_alloc(&slot, TC * NCH);  // first: releases the allocation permit early
   const uint32_t a1s = smem_u32(sA1[ch]), ws = smem_u32(sW);
@@ -186,14 +193,14 @@ __global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2
     load(pi);  // next tile's features in flight during this tile's chain
     fence_async_smem();
     tc_fence_before();
-    stc_chain_sync(ch);
+    stc_chain_sync<NCH>(ch);
     if (wq == 0) {
       tc_fence_after();
       mma_tf32_ss_elect(tb, a1d, w1d, id1, 0);
       mma_commit_elect(&bar[ch][0]);
       mbar_wait_sleep(&bar[ch][0], it & 1);  // the issuing warp waits; the others sleep in the barrier
     }
-    stc_chain_sync(ch);
+    stc_chain_sync<NCH>(ch);
     tc_fence_after();
     // ---- layer-1 epilogue: act + bf16 pairs back into this lane's columns (layer 2's A)
 #pragma unroll
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2
     }
     tmem_wait_st();
     tc_fence_before();
-    stc_chain_sync(ch);
+    stc_chain_sync<NCH>(ch);
     if (wq == 0) {
       tc_fence_after();
 #pragma unroll
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2
       mma_commit_elect(&bar[ch][1]);
       mbar_wait_sleep(&bar[ch][1], it & 1);
     }
-    stc_chain_sync(ch);
+    stc_chain_sync<NCH>(ch);
     tc_fence_after();
     // ---- layer-2 epilogue: act(acc2 + b2) as bf16 pairs into this lane's
     // A3 columns, then one N = 16 TS MMA chain (K = N2) gives the G outputs
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2
     }
     tmem_wait_st();
     tc_fence_before();
-    stc_chain_sync(ch);
+    stc_chain_sync<NCH>(ch);
     if (wq == 0) {
       tc_fence_after();
 #pragma unroll
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(128 * stc_chains(N1, N2), stc_sm_chains(N1, N2
       mma_commit_elect(&bar[ch][2]);
       mbar_wait_sleep(&bar[ch][2], it & 1);
     }
-    stc_chain_sync(ch);
+    stc_chain_sync<NCH>(ch);
     tc_fence_after();
     float y[GP];
     {
