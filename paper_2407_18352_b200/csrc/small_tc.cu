@@ -63,7 +63,7 @@ __host__ __device__ constexpr int stc_cols(int n1, int n2) {
 }
 // 128-row chains per SM (all of TMEM, at most 8) and per CTA (STC_CPS)
 #ifndef STC_CPS
-#define STC_CPS 1  // measured on C1 bf16: 1 / 2 / 4 / 8 chains per CTA = 22.2 / 22.6 / 23.1 / 24.6 us (before the uniform warp index)
+#define STC_CPS 1  // C1 bf16: 1 / 2 / 8 chains per CTA equal (18.5 us); before the uniform warp index 1 was fastest
 #endif
 __host__ __device__ constexpr int stc_sm_chains(int n1, int n2) {
   return 512 / stc_cols(n1, n2) < 8 ? 512 / stc_cols(n1, n2) : 8;
