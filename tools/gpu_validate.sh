@@ -11,3 +11,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:sma
     -o gpurun_out/r02/prof_options_bf16 -f python bench.py --config options_bf16 --steps 1 --warmup 2 --no-e2e --no-cpu --no-parity --no-per-config > gpurun_out/r02/prof_options_bf16.log 2>&1; echo "ncu rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/r02/launches_options_bf16.csv python bench.py --config options_bf16 --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity --no-per-config > /dev/null 2>&1; echo "launches rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:w4_fused" -s 2 -c 1 \
+    -o gpurun_out/r02/prof_minibude_w4 -f python bench.py --config minibude --steps 1 --warmup 2 --no-e2e --no-cpu --no-parity --no-per-config > gpurun_out/r02/prof_minibude_w4.log 2>&1; echo "ncu w4 rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/r02/launches_minibude.csv python bench.py --config minibude --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity --no-per-config > /dev/null 2>&1; echo "launches minibude rc=$?"
