@@ -32,7 +32,8 @@ using namespace ptx;
 
 constexpr int GBM = 128;
 constexpr int GTHREADS = 192;
-enum { EPI_BF16 = 0, EPI_DOT = 1, EPI_F32 = 2 };
+enum { EPI_BF16 = 0, EPI_DOT = 1, EPI_F32 = 2, EPI_DOTG = 3 };
+constexpr int DOTG_MAX = 4;  // EPI_DOTG: outputs of the fused last layer
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -76,6 +77,12 @@ struct GemmArgs {
   float* staged;           // checked commit: staged[row - r_stage0]
   int64_t r_stage0;
   uint32_t* status;
+  // EPI_DOTG (generic chain, last layer fused into the one before it):
+  // y[m][o] = act_last(sum_n bf16(act(acc + bias[n])) * w_last[o][n] + b_last[o]),
+  // f32 rows of g_out into out_f32 (row stride ldo)
+  const __nv_bfloat16* w_last;  // [>= g_out][k_last] bf16 (the chain blob's layer)
+  const float* b_last;
+  int g_out, k_last, act_last;
 };
 
 struct OutPtrs {
@@ -178,6 +185,17 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
 #pragma unroll
           for (int j = 0; j < 4; ++j) o[j] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
         }
+      } else if constexpr (EPI == EPI_DOTG) {
+        // the hidden activations rounded to bf16 (the chain's quantisation
+        // point between layers), dotted with the last layer's bf16 weights
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int n = n0 + e;
+          const float h = __bfloat162float(__float2bfloat16_rn(act_g<ACT>(__uint_as_float(v[e]) + bias_s[n])));
+#pragma unroll
+          for (int o = 0; o < DOTG_MAX; ++o)
+            if (o < g.g_out) acc[o] = fmaf(h, __bfloat162float(g.w_last[(int64_t)o * g.k_last + n]), acc[o]);
+        }
       } else {
 #if SMLRT_GEMM_EPI_PACKED
         if constexpr (ACT != SMLRT_TANH) {
@@ -225,6 +243,22 @@ __device__ __forceinline__ void gemm_epilogue(uint32_t tbase, uint64_t* tfull, u
         }
         consume(v, c0);
       }
+    }
+    if constexpr (EPI == EPI_DOTG) {
+      bool bad = false;
+      if (m < g.M) {
+        float* o = g.out_f32 + m * g.ldo;
+#pragma unroll
+        for (int k = 0; k < DOTG_MAX; ++k)
+          if (k < g.g_out) {
+            float y = acc[k] + g.b_last[k];
+            if (g.act_last == SMLRT_RELU) y = act_g<SMLRT_RELU>(y);
+            else if (g.act_last == SMLRT_TANH) y = tanhf(y);
+            bad |= (__float_as_uint(y) & 0x7f800000u) == 0x7f800000u;
+            o[k] = y;
+          }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) flag_nonfinite(g.status);
     }
     if constexpr (EPI == EPI_DOT) {
       for (int p = 0; p < 4; ++p) {
@@ -1694,6 +1728,15 @@ int chain_max_width(const smlrt_model_s& m) {
   return w;
 }
 
+// SMLRT_CHAIN_FUSE_LAST=0: the last layer as its own GEMM (A/B switch)
+bool chain_fuse_last() {
+  static const int v = [] {
+    const char* e = std::getenv("SMLRT_CHAIN_FUSE_LAST");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 // the chain's GEMMs over n rows whose bf16 layer-0 activations are in act0
 // ([n][k_pad0]); act1 is a second [n][max_width] buffer; the last layer
 // writes f32 [n][G] rows into y
@@ -1706,8 +1749,28 @@ int chain_forward(const smlrt_model_s& m, __nv_bfloat16* act0, __nv_bfloat16* ac
   __nv_bfloat16* cur = act0;
   __nv_bfloat16* nxt = act1;
   const int nl = (int)m.chain.size();
+  // a last layer of <= 4 outputs rides in the previous layer's epilogue when
+  // that layer is one N tile (no f32 round trip, one GEMM launch less)
+  const bool fuse_last = chain_fuse_last() && nl >= 2 && m.chain[nl - 1].n <= DOTG_MAX &&
+                         (m.chain[nl - 2].n_pad == 64 || m.chain[nl - 2].n_pad == 128 || m.chain[nl - 2].n_pad == 256);
   for (int l = 0; l < nl; ++l) {
     const auto& c = m.chain[l];
+    if (fuse_last && l == nl - 2) {
+      const auto& c2 = m.chain[nl - 1];
+      GemmArgs g{};
+      g.M = (int)n;
+      g.act = c.act;
+      g.bias = reinterpret_cast<const float*>(wb + c.b_off);
+      g.status = status;
+      g.out_f32 = y;
+      g.ldo = G;
+      g.w_last = reinterpret_cast<const __nv_bfloat16*>(wb + c2.w_off);
+      g.b_last = reinterpret_cast<const float*>(wb + c2.b_off);
+      g.g_out = c2.n;
+      g.k_last = c2.k_pad;
+      g.act_last = c2.act;
+      return chain_gemm<EPI_DOTG>(cur, c.k_pad, wb + c.w_off, c.k_pad, c.n_pad, g, none, dst, s);
+    }
     GemmArgs g{};
     g.M = (int)n;
     g.act = c.act;

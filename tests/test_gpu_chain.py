@@ -127,3 +127,19 @@ def test_chain_nonfinite_raises(cuda, tmp_path):
         with pytest.raises(NonFiniteOutputError):
             rt.invoke_region(rt.register_region(desc))
     assert (yb.to_numpy() == 0).all()  # checked commit: nothing written
+
+
+def test_chain_unfused_last_layer(cuda):
+    """A last layer of <= 4 outputs runs in the previous GEMM's epilogue
+    (EPI_DOTG: bf16 hidden activations dotted with the bf16 last-layer
+    weights); SMLRT_CHAIN_FUSE_LAST=0 (read once per process) keeps it a
+    GEMM of its own: the shape cases re-run in a subprocess with it off."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("SMLRT_CHAIN_FUSE_LAST") == "0":
+        pytest.skip("already the unfused run")
+    env = dict(os.environ, SMLRT_CHAIN_FUSE_LAST="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "chain_shapes"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

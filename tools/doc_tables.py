@@ -28,7 +28,7 @@ ROWS = [  # (label, config, kernels, bound text, parity sample)
     ("C4 ParticleFilter 16,384 windows, CNN fp32", "particlefilter",
      "`conv_pool_k8oc8_kernel` + `dense_pair_kernel<1>` + row scatter", "of FP32", "2,048 frames"),
     ("C4 at bf16 (`particlefilter_bf16`)", "particlefilter_bf16",
-     "same conv front (bf16 features) + tcgen05 chain GEMMs 512→128→2 + scatter", "of HBM", "2,048 frames"),
+     "same conv front (bf16 features) + tcgen05 GEMM 512→128 with the 128→2 layer in its epilogue + scatter", "of HBM", "2,048 frames"),
     ("C5 MiniWeather 4094×2046, 36-8-4 fp32", "miniweather", "`stencil_exact_kernel` (TMA ring)", "of FP32",
      "all 8.4M points"),
     ("C5 at bf16 (`miniweather_bf16`)", "miniweather_bf16", "`stencil_mma_kernel` (TMA ring + warp MMAs)", "of HBM",
